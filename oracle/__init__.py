@@ -1,0 +1,290 @@
+"""CPU oracle for the SageAttention3 FP4 attention forward (arXiv 2505.11594, Algorithm 1).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The product package
+(``paper_2505_11594_b200``) never imports it, and the two share no code.
+
+The arithmetic lives in ``sage3_oracle.c`` (plain C, fp64 except where the paper fixes fp32); this
+module is a ctypes binding plus the paper's accuracy metrics (Appendix).  Every function
+documents the passage it follows; readings of ambiguous points are SURVEY.md §8(c) c1-c16, copied into
+DESIGN.md §3.
+
+Parity status: codecs, φ, K-mean, FP4MM, two-level P and the online-softmax recurrence
+are each pinned by tests/test_oracle_*.py to tables, closed forms, library routines or the plain
+definition of attention.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sage3_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_CFLAGS = ["-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC"]
+_lock = threading.Lock()
+_lib = None
+
+PMODE_TWO_LEVEL, PMODE_DIRECT, PMODE_NONE = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no fast-math, no FMA contraction, no FTZ/DAZ)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.run(["gcc", *_CFLAGS, _SRC, "-o", tmp, "-lm"], check=True)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = ctypes.CDLL(build())
+            u8p = ctypes.POINTER(ctypes.c_uint8)
+            fp = ctypes.POINTER(ctypes.c_float)
+            dp = ctypes.POINTER(ctypes.c_double)
+            ip = ctypes.POINTER(ctypes.c_int)
+            L.oracle_e2m1_encode.restype = ctypes.c_uint8
+            L.oracle_e2m1_encode.argtypes = [ctypes.c_float]
+            L.oracle_e2m1_decode.restype = ctypes.c_double
+            L.oracle_e2m1_decode.argtypes = [ctypes.c_uint8]
+            L.oracle_e4m3_encode.restype = ctypes.c_uint8
+            L.oracle_e4m3_encode.argtypes = [ctypes.c_float]
+            L.oracle_e4m3_decode.restype = ctypes.c_double
+            L.oracle_e4m3_decode.argtypes = [ctypes.c_uint8]
+            L.oracle_enumerate.restype = ctypes.c_int
+            L.oracle_enumerate.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, dp]
+            L.oracle_phi_nvfp4.argtypes = [fp, u8p, u8p]
+            L.oracle_phi_mxfp4.argtypes = [fp, u8p, u8p]
+            L.oracle_kmean.argtypes = [fp, ctypes.c_int, ctypes.c_int, fp]
+            L.oracle_quantize_head.argtypes = [fp, fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               u8p, u8p, u8p, u8p, u8p, u8p, fp]
+            L.oracle_dequant.argtypes = [u8p, u8p, ctypes.c_int, ctypes.c_int, dp]
+            L.oracle_fp4mm.argtypes = [u8p, u8p, u8p, u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
+            L.oracle_two_level_row.restype = ctypes.c_float
+            L.oracle_two_level_row.argtypes = [fp, ctypes.c_int, ctypes.c_int, u8p, u8p]
+            L.oracle_attn_fwd.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ip,
+                                          ctypes.c_int, dp, dp]
+            L.oracle_attn_fwd_float.argtypes = [ctypes.c_int, ctypes.c_int, fp, fp, fp, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_double, ctypes.c_int, ip, ctypes.c_int, dp, dp]
+            L.oracle_reference_attention.argtypes = [ctypes.c_int, ctypes.c_int, fp, fp, fp, ctypes.c_int,
+                                                     ctypes.c_double, ip, ctypes.c_int, dp]
+            L.oracle_num_threads.restype = ctypes.c_int
+            L.oracle_e2m1_encode_array.argtypes = [fp, ctypes.c_int64, u8p]
+            L.oracle_e4m3_encode_array.argtypes = [fp, ctypes.c_int64, u8p]
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray, ct):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+# ---------------------------------------------------------------------------------------- codecs
+def e2m1_encode(x: float) -> int:
+    """E2M1 round-to-nearest-even, saturating, sign kept (reading c1)."""
+    return int(lib().oracle_e2m1_encode(float(np.float32(x))))
+
+
+def e2m1_decode(c: int) -> float:
+    return float(lib().oracle_e2m1_decode(int(c)))
+
+
+def e4m3_encode(x: float) -> int:
+    """E4M3 round-to-nearest-even, saturating at 448, never NaN (reading c2)."""
+    return int(lib().oracle_e4m3_encode(float(np.float32(x))))
+
+
+def e4m3_decode(c: int) -> float:
+    return float(lib().oracle_e4m3_decode(int(c)))
+
+
+def e2m1_encode_array(x) -> np.ndarray:
+    x = _f32(x).ravel()
+    out = np.zeros(x.shape[0], np.uint8)
+    lib().oracle_e2m1_encode_array(_p(x, ctypes.c_float), x.shape[0], _p(out, ctypes.c_uint8))
+    return out
+
+
+def e4m3_encode_array(x) -> np.ndarray:
+    x = _f32(x).ravel()
+    out = np.zeros(x.shape[0], np.uint8)
+    lib().oracle_e4m3_encode_array(_p(x, ctypes.c_float), x.shape[0], _p(out, ctypes.c_uint8))
+    return out
+
+
+def enumerate_values(fmt: str, lo: float, hi: float) -> np.ndarray:
+    """Distinct representable values in [lo, hi] (appendix)."""
+    out = np.zeros(256, dtype=np.float64)
+    n = lib().oracle_enumerate(0 if fmt == "e2m1" else 1, lo, hi, _p(out, ctypes.c_double))
+    return out[:n].copy()
+
+
+def phi_nvfp4(x) -> tuple[np.ndarray, int]:
+    """φ on one 1x16 block (Eq. 1): returns (16 E2M1 codes, E4M3 scale code)."""
+    x = _f32(x)
+    assert x.shape == (16,)
+    codes = np.zeros(16, dtype=np.uint8)
+    sc = np.zeros(1, dtype=np.uint8)
+    lib().oracle_phi_nvfp4(_p(x, ctypes.c_float), _p(codes, ctypes.c_uint8), _p(sc, ctypes.c_uint8))
+    return codes, int(sc[0])
+
+
+def phi_mxfp4(x) -> tuple[np.ndarray, int]:
+    """MXFP4 ablation φ on one 1x32 block (E8M0 rounded up)."""
+    x = _f32(x)
+    assert x.shape == (32,)
+    codes = np.zeros(32, dtype=np.uint8)
+    sc = np.zeros(1, dtype=np.uint8)
+    lib().oracle_phi_mxfp4(_p(x, ctypes.c_float), _p(codes, ctypes.c_uint8), _p(sc, ctypes.c_uint8))
+    return codes, int(sc[0])
+
+
+def e2m1_table() -> np.ndarray:
+    return np.array([e2m1_decode(c) for c in range(16)])
+
+
+def e4m3_table() -> np.ndarray:
+    return np.array([e4m3_decode(c) for c in range(256)])
+
+
+def dequant(codes: np.ndarray, sf: np.ndarray) -> np.ndarray:
+    """φ^-1 (Eq. 2) for codes [R][C] with scales [R][C/16]; exact fp64."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    sf = np.ascontiguousarray(sf, dtype=np.uint8)
+    R, C = codes.shape
+    out = np.zeros((R, C), dtype=np.float64)
+    lib().oracle_dequant(_p(codes, ctypes.c_uint8), _p(sf, ctypes.c_uint8), R, C, _p(out, ctypes.c_double))
+    return out
+
+
+def fp4mm(a_codes, a_sf, b_codes, b_sf) -> np.ndarray:
+    """FP4MM (Eq. 3): φ^-1(A) φ^-1(B)^T, A [M][K], B [N][K] (both blocked along K)."""
+    a_codes = np.ascontiguousarray(a_codes, dtype=np.uint8)
+    b_codes = np.ascontiguousarray(b_codes, dtype=np.uint8)
+    a_sf = np.ascontiguousarray(a_sf, dtype=np.uint8)
+    b_sf = np.ascontiguousarray(b_sf, dtype=np.uint8)
+    M, K = a_codes.shape
+    N = b_codes.shape[0]
+    out = np.zeros((M, N), dtype=np.float64)
+    lib().oracle_fp4mm(_p(a_codes, ctypes.c_uint8), _p(a_sf, ctypes.c_uint8), _p(b_codes, ctypes.c_uint8),
+                       _p(b_sf, ctypes.c_uint8), M, N, K, _p(out, ctypes.c_double))
+    return out
+
+
+def two_level_row(P, p_mode: int = PMODE_TWO_LEVEL):
+    """Two-level quantization of one row of P̃ (§3.2): returns (s_P1, codes, s_P2 codes)."""
+    P = _f32(P)
+    n = P.shape[0]
+    codes = np.zeros(n, dtype=np.uint8)
+    sf = np.zeros(n // 16, dtype=np.uint8)
+    s = lib().oracle_two_level_row(_p(P, ctypes.c_float), n, p_mode, _p(codes, ctypes.c_uint8),
+                                   _p(sf, ctypes.c_uint8))
+    return float(np.float32(s)), codes, sf
+
+
+def kmean(K) -> np.ndarray:
+    """Smoothing-K mean (Alg1 L2) in the fixed order of reading c10."""
+    K = _f32(K)
+    N, d = K.shape
+    km = np.zeros(d, dtype=np.float32)
+    lib().oracle_kmean(_p(K, ctypes.c_float), N, d, _p(km, ctypes.c_float))
+    return km
+
+
+class QuantizedHead:
+    """Logical-layout NVFP4 codes of one head (one code per byte): q/k [Np][d], v [d][Np]."""
+
+    def __init__(self, N, d):
+        Np = (N + 127) // 128 * 128
+        self.N, self.d, self.Np = N, d, Np
+        self.q_codes = np.zeros((Np, d), np.uint8)
+        self.k_codes = np.zeros((Np, d), np.uint8)
+        self.v_codes = np.zeros((d, Np), np.uint8)
+        self.q_sf = np.zeros((Np, d // 16), np.uint8)
+        self.k_sf = np.zeros((Np, d // 16), np.uint8)
+        self.v_sf = np.zeros((d, Np // 16), np.uint8)
+        self.km = np.zeros(d, np.float32)
+
+
+def quantize_head(Q, K, V, smooth_k: bool = True) -> QuantizedHead:
+    """Alg1 L2 (smoothing K) + φ of Q, K (along d) and V (along tokens, stored transposed)."""
+    Q, K, V = _f32(Q), _f32(K), _f32(V)
+    N, d = Q.shape
+    h = QuantizedHead(N, d)
+    u8 = ctypes.c_uint8
+    lib().oracle_quantize_head(_p(Q, ctypes.c_float), _p(K, ctypes.c_float), _p(V, ctypes.c_float), N, d,
+                               1 if smooth_k else 0, _p(h.q_codes, u8), _p(h.q_sf, u8), _p(h.k_codes, u8),
+                               _p(h.k_sf, u8), _p(h.v_codes, u8), _p(h.v_sf, u8), _p(h.km, ctypes.c_float))
+    return h
+
+
+def attn_fwd(heads: list[QuantizedHead], *, causal: bool, scale: float, rows=None, bkv: int = 128,
+             p_mode: int = PMODE_TWO_LEVEL, want_lse: bool = False):
+    """Alg1 L6-L13 on quantized heads (all same N, d).  Returns O [BH][nrows][d] fp64 (and lse)."""
+    N, d, Np = heads[0].N, heads[0].d, heads[0].Np
+    BH = len(heads)
+    rows = np.arange(N, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    cat = lambda name: np.ascontiguousarray(np.stack([getattr(h, name) for h in heads]))
+    qc, qs, kc, ks, vc, vs = (cat(n) for n in ("q_codes", "q_sf", "k_codes", "k_sf", "v_codes", "v_sf"))
+    O = np.zeros((BH, rows.shape[0], d), np.float64)
+    lse = np.zeros((BH, rows.shape[0]), np.float64)
+    u8 = ctypes.c_uint8
+    lib().oracle_attn_fwd(BH, N, d, _p(qc, u8), _p(qs, u8), _p(kc, u8), _p(ks, u8), _p(vc, u8), _p(vs, u8), bkv,
+                          1 if causal else 0, float(scale), p_mode, _p(rows, ctypes.c_int), rows.shape[0],
+                          _p(O, ctypes.c_double), _p(lse, ctypes.c_double))
+    return (O, lse) if want_lse else O
+
+
+def attn_fwd_float(Q, K, V, *, causal: bool, scale: float, rows=None, bkv: int = 128,
+                   p_mode: int = PMODE_NONE, want_lse: bool = False):
+    """The same tiled recurrence on unquantized inputs (p_mode NONE = FlashAttention in fp64)."""
+    Q, K, V = _f32(Q), _f32(K), _f32(V)
+    N, d = Q.shape
+    rows = np.arange(N, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    O = np.zeros((rows.shape[0], d), np.float64)
+    lse = np.zeros(rows.shape[0], np.float64)
+    fp = ctypes.c_float
+    lib().oracle_attn_fwd_float(N, d, _p(Q, fp), _p(K, fp), _p(V, fp), bkv, 1 if causal else 0, float(scale),
+                                p_mode, _p(rows, ctypes.c_int), rows.shape[0], _p(O, ctypes.c_double),
+                                _p(lse, ctypes.c_double))
+    return (O, lse) if want_lse else O
+
+
+def reference_attention(Q, K, V, *, causal: bool, scale: float, rows=None) -> np.ndarray:
+    """Plain fp64 softmax attention on the original inputs, for the accuracy metrics."""
+    Q, K, V = _f32(Q), _f32(K), _f32(V)
+    N, d = Q.shape
+    rows = np.arange(N, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    O = np.zeros((rows.shape[0], d), np.float64)
+    fp = ctypes.c_float
+    lib().oracle_reference_attention(N, d, _p(Q, fp), _p(K, fp), _p(V, fp), 1 if causal else 0, float(scale),
+                                     _p(rows, ctypes.c_int), rows.shape[0], _p(O, ctypes.c_double))
+    return O
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+# ---------------------------------------------------------------------------------------- metrics
+def accuracy_metrics(ref, test) -> dict:
+    """Appendix metrics: CosSim = ΣOO'/(√ΣO²√ΣO'²), L1 = Σ|O-O'|/Σ|O|, RMSE = √(mean (O-O')²)."""
+    a = np.asarray(ref, dtype=np.float64).ravel()
+    b = np.asarray(test, dtype=np.float64).ravel()
+    cos = float(np.dot(a, b) / (np.sqrt(np.dot(a, a)) * np.sqrt(np.dot(b, b))))
+    l1 = float(np.abs(a - b).sum() / np.abs(a).sum())
+    rmse = float(np.sqrt(np.mean((a - b) ** 2)))
+    return {"cos_sim": cos, "l1": l1, "rmse": rmse}
