@@ -1,0 +1,130 @@
+/*
+ * sage3.h — C ABI of the B200 (sm_100a) SageAttention3 FP4 attention forward (arXiv 2505.11594).
+ *
+ * The library implements the north_star hot path: Algorithm 1 of the paper
+ * without smoothing Q:
+ *   sage3_quantize_qkv : Alg1 L2 (K -= mean(K)) and L7 (φ of Q, K along d; φ of V along tokens,
+ *                        stored transposed) — NVFP4 = E2M1 codes + E4M3 per-16 scales
+ *                        (P:129), φ as Eq. 1.
+ *   sage3_attn_fwd     : Alg1 L6-L13 — S = FP4MM(Q̂,s_Q,K̂,s_K) (Eq. 3), online softmax (L9),
+ *                        two-level P quantization (L10, §3.2), O += FP4MM(P̂2,s_P2,V̂,s_V)·s_P1
+ *                        (L11), O = diag(l)^-1 O (L13).
+ * The readings of points the paper leaves open (rounding, softmax scale, causal mask, padding) are
+ * listed in DESIGN.md §3; the numerics are bit-exact (quantizer) / within tolerance (attention) of the
+ * CPU oracle in oracle/.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless the name says _host.  The caller allocates and owns every
+ *    buffer; the library never allocates or frees device memory.
+ *  - Every call only enqueues work on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *    stream) on the CURRENT device; nothing synchronizes, except sage3_forward_host which also enqueues
+ *    its copies and returns without synchronizing.
+ *  - Argument errors are detected on the host before anything is enqueued and returned as a status;
+ *    launch failures return SAGE3_ERR_CUDA (see sage3_last_cuda_error).  Device faults surface at the
+ *    caller's next synchronization.  No C++ exception crosses the ABI.
+ *  - Inputs must be finite.  A violation is reported through the optional device flag of
+ *    sage3_quantize_qkv, not trapped.
+ *  - Thread safety: stateless apart from per-device one-time kernel attribute setup; safe to call
+ *    concurrently from threads that drive different devices.
+ */
+#ifndef SAGE3_H_
+#define SAGE3_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SAGE3_OK = 0,
+  SAGE3_ERR_INVALID_ARG = 1, /* null pointer, B/H/N < 1, d not in {64,128}, stride/alignment violation  */
+  SAGE3_ERR_UNSUPPORTED = 2, /* current device is not compute capability 10.0 (sm_100a), bad dtype      */
+  SAGE3_ERR_WORKSPACE = 3,   /* workspace / scratch smaller than the *_bytes query returned            */
+  SAGE3_ERR_CUDA = 4         /* a CUDA launch or driver call failed; see sage3_last_cuda_error()        */
+} sage3_status;
+
+typedef enum { SAGE3_FP16 = 0, SAGE3_BF16 = 1, SAGE3_FP32 = 2 /* output only */ } sage3_dtype;
+
+/* A [B][H][N][d] tensor: element (b,h,n,c) is at ptr + b*stride_b + h*stride_h + n*stride_n + c
+ * (strides in ELEMENTS; the d stride is 1).  ptr and every stride*sizeof(elem) must be 16-byte aligned. */
+typedef struct {
+  void* ptr;
+  int64_t stride_b, stride_h, stride_n;
+} sage3_tensor4;
+
+/* NVFP4 Q, K, V of one call, produced by sage3_quantize_qkv and consumed by sage3_attn_fwd.
+ * N_pad = round_up(N, 128).  Codes: E2M1, two per byte, element 2k in the LOW nibble.
+ *   q_data, k_data : [B][H][N_pad][d/2]     blocks of 16 along d (the QK^T reduction dim)
+ *   v_data         : [B][H][d][N_pad/2]     V transposed: tokens contiguous, blocks of 16 tokens
+ * Scales: E4M3 (UE4M3, sign 0), one per 16-element block, in 512-byte SF atoms of 128 rows x 4 blocks:
+ *   byte(r, c) = ((r/128)*(C/4) + c/4)*512 + (r%32)*16 + ((r/32)%4)*4 + (c%4)      per (b,h) matrix
+ *   q_sf, k_sf : R = N_pad rows (tokens), C = d/16 blocks;       N_pad*d/16 bytes per (b,h)
+ *   v_sf       : R = 128 rows (channels, rows >= d are zero), C = N_pad/16;  8*N_pad bytes per (b,h)
+ *   (the layout tcgen05.cp.32x128b.warpx4 expects; identical to cuBLAS's VEC16_UE4M3 layout)
+ * Padding tokens n in [N, N_pad) hold zero codes and zero scales.
+ *   k_mean : [B][H][d] fp32, the smoothing-K mean (Alg1 L2). */
+typedef struct {
+  int32_t B, H, N, d, N_pad;
+  uint8_t* q_data;
+  uint8_t* k_data;
+  uint8_t* v_data;
+  uint8_t* q_sf;
+  uint8_t* k_sf;
+  uint8_t* v_sf;
+  float* k_mean;
+} sage3_fp4_qkv;
+
+/* Host-only size queries (no CUDA calls).  bytes[0..6] = q_data, k_data, v_data, q_sf, k_sf, v_sf,
+ * k_mean.  Returns SAGE3_ERR_INVALID_ARG for unsupported shapes. */
+sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]);
+
+/* Device workspace of sage3_quantize_qkv: fp64 K-mean partial sums, B*H*(N_pad/128)*d*8 bytes. */
+size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d);
+
+/* B_kv (keys per tile) used by sage3_attn_fwd for head dim d.  The per-tile first-level P scale s_P1
+ * (Alg1 L10) makes the result depend on it, so the oracle must use the same value.  Returns 128, or 0
+ * for an unsupported d. */
+int sage3_kv_tile(int d);
+
+/* Alg1 L2 + L7.  q, k, v: [B][H][N][d] in `in_dtype` (SAGE3_FP16 or SAGE3_BF16).  Fills every array of
+ * *out (whose pointers and B,H,N,d fields the caller sets; N_pad is written).  `workspace` must hold
+ * sage3_quantize_workspace_bytes().  nonfinite_flag: nullable device u32, OR-set to 1 if any input is
+ * NaN/Inf (the codes are then unspecified).
+ * Numerics (bit-exact with oracle_quantize_head): km[c] = fl32(Σ_chunks Σ_tokens K / N) in fp64 with the
+ * fixed order of DESIGN.md reading c10; x = fl32(K - km); s = E4M3_RNE(fl32(amax·fl32(1/6)));
+ * codes = E2M1_RNE(fl32(x·fl32(1/s))), all-zero codes when s == 0. */
+sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 v, sage3_dtype in_dtype, int B,
+                                int H, int N, int d, sage3_fp4_qkv* out, void* workspace, size_t workspace_bytes,
+                                uint32_t* nonfinite_flag, void* stream);
+
+/* Alg1 L6-L13 on the NVFP4 tensors of *qkv.  o: [B][H][N][d] in o_dtype (FP16, BF16 or FP32); rows
+ * n >= N are never written.  causal != 0: key j is visible to query i iff j <= i (top-left aligned).
+ * softmax_scale <= 0 selects 1/sqrt(d); S is scaled after the MMA: P̃ = exp(scale·(S - m)).
+ * lse: nullable device fp32 [B][H][N], lse = scale·m + ln(l) (natural log).
+ * The tensor-core path: tcgen05.mma.kind::mxf4nvf4.block_scale (scale_vec::4X) for QK^T and PV with
+ * fp32 accumulators and scale factors in TMEM, TMA-staged operands, B_q = B_kv = 128. */
+sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                            float softmax_scale, float* lse, void* stream);
+
+/* End-to-end convenience path with HOST buffers (for e2e measurements): copies contiguous host
+ * q, k, v ([B][H][N][d], in_dtype; pinned memory recommended) to device scratch, quantizes, runs the
+ * attention and copies O (contiguous [B][H][N][d], o_dtype) back to o_host — all enqueued on `stream`;
+ * the caller synchronizes the stream before reading o_host.  `scratch` (device) must hold
+ * sage3_forward_host_scratch_bytes(). */
+size_t sage3_forward_host_scratch_bytes(int B, int H, int N, int d, sage3_dtype in_dtype, sage3_dtype o_dtype);
+sage3_status sage3_forward_host(const void* q_host, const void* k_host, const void* v_host, sage3_dtype in_dtype,
+                                int B, int H, int N, int d, int causal, float softmax_scale, void* o_host,
+                                sage3_dtype o_dtype, void* scratch, size_t scratch_bytes, void* stream);
+
+const char* sage3_status_str(sage3_status s);
+/* cudaError_t (as int) of the last SAGE3_ERR_CUDA returned on this host thread; 0 if none. */
+int sage3_last_cuda_error(void);
+/* Library version string, e.g. "sage3-b200 0.1 sm_100a". */
+const char* sage3_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAGE3_H_ */

@@ -1,0 +1,193 @@
+"""B200-native (sm_100a) SageAttention3 FP4 attention forward — thin ctypes binding over libsage3.so.
+
+The C ABI is ``include/sage3.h``; the functions here carry the same names and only marshal arguments
+(torch tensors -> device pointers / strides, the current CUDA stream).  Every step of the method runs in
+the CUDA kernels of ``csrc/``; there is no CPU or PyTorch fallback: if the library is missing this
+module raises.  PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsage3.so")
+
+SAGE3_OK, SAGE3_ERR_INVALID_ARG, SAGE3_ERR_UNSUPPORTED, SAGE3_ERR_WORKSPACE, SAGE3_ERR_CUDA = range(5)
+SAGE3_FP16, SAGE3_BF16, SAGE3_FP32 = 0, 1, 2
+_DT = {torch.float16: SAGE3_FP16, torch.bfloat16: SAGE3_BF16, torch.float32: SAGE3_FP32}
+
+# Every function include/sage3.h declares (checked by tests/test_abi.py).
+ABI_FUNCTIONS = (
+    "sage3_fp4_qkv_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
+    "sage3_attn_fwd", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
+    "sage3_last_cuda_error", "sage3_version",
+)
+
+
+class Sage3Error(RuntimeError):
+    pass
+
+
+class Tensor4(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("stride_b", ctypes.c_int64), ("stride_h", ctypes.c_int64),
+                ("stride_n", ctypes.c_int64)]
+
+
+class FP4QKVStruct(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("N", ctypes.c_int32), ("d", ctypes.c_int32),
+                ("N_pad", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in (
+                    "q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean")]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libsage3.so (built in-tree by ``python -m paper_2505_11594_b200.build``); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise Sage3Error(f"{LIB_PATH} is missing: build it with `python -m paper_2505_11594_b200.build` "
+                         "(there is no fallback implementation)")
+    L = ctypes.CDLL(LIB_PATH)
+    sz = ctypes.c_size_t
+    L.sage3_fp4_qkv_sizes.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(sz)]
+    L.sage3_quantize_workspace_bytes.argtypes = [ctypes.c_int] * 4
+    L.sage3_quantize_workspace_bytes.restype = sz
+    L.sage3_kv_tile.argtypes = [ctypes.c_int]
+    L.sage3_quantize_qkv.argtypes = [Tensor4, Tensor4, Tensor4, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.POINTER(FP4QKVStruct), ctypes.c_void_p, sz,
+                                     ctypes.c_void_p, ctypes.c_void_p]
+    L.sage3_attn_fwd.argtypes = [ctypes.POINTER(FP4QKVStruct), Tensor4, ctypes.c_int, ctypes.c_int, ctypes.c_float,
+                                 ctypes.c_void_p, ctypes.c_void_p]
+    L.sage3_forward_host_scratch_bytes.argtypes = [ctypes.c_int] * 6
+    L.sage3_forward_host_scratch_bytes.restype = sz
+    L.sage3_forward_host.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 6 + [ctypes.c_float, ctypes.c_void_p,
+                                                                                ctypes.c_int, ctypes.c_void_p, sz,
+                                                                                ctypes.c_void_p]
+    L.sage3_status_str.argtypes = [ctypes.c_int]
+    L.sage3_status_str.restype = ctypes.c_char_p
+    L.sage3_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(status: int, what: str):
+    if status != SAGE3_OK:
+        L = load()
+        msg = L.sage3_status_str(status).decode()
+        if status == SAGE3_ERR_CUDA:
+            msg += f" (cudaError {L.sage3_last_cuda_error()})"
+        raise Sage3Error(f"{what}: {msg}")
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _t4(x: torch.Tensor) -> Tensor4:
+    assert x.dim() == 4 and x.stride(3) == 1, "expected [B, H, N, d] with unit d-stride"
+    return Tensor4(x.data_ptr(), x.stride(0), x.stride(1), x.stride(2))
+
+
+def version() -> str:
+    return load().sage3_version().decode()
+
+
+def sage3_kv_tile(d: int) -> int:
+    return int(load().sage3_kv_tile(d))
+
+
+def sage3_fp4_qkv_sizes(B: int, H: int, N: int, d: int) -> list[int]:
+    out = (ctypes.c_size_t * 7)()
+    _check(load().sage3_fp4_qkv_sizes(B, H, N, d, out), "sage3_fp4_qkv_sizes")
+    return list(out)
+
+
+def sage3_quantize_workspace_bytes(B: int, H: int, N: int, d: int) -> int:
+    return int(load().sage3_quantize_workspace_bytes(B, H, N, d))
+
+
+class FP4QKV:
+    """Device buffers of one NVFP4 Q/K/V set (layouts: include/sage3.h), allocated with torch."""
+
+    NAMES = ("q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean")
+
+    def __init__(self, B: int, H: int, N: int, d: int, device):
+        self.B, self.H, self.N, self.d = B, H, N, d
+        self.N_pad = (N + 127) // 128 * 128
+        sizes = sage3_fp4_qkv_sizes(B, H, N, d)
+        for name, nbytes in zip(self.NAMES, sizes):
+            setattr(self, name, torch.empty(nbytes, dtype=torch.uint8, device=device))
+        self.workspace = torch.empty(max(sage3_quantize_workspace_bytes(B, H, N, d), 16), dtype=torch.uint8,
+                                     device=device)
+        self.struct = FP4QKVStruct(B, H, N, d, self.N_pad,
+                                   *[getattr(self, n).data_ptr() for n in self.NAMES])
+
+    def nbytes(self) -> int:
+        return sum(getattr(self, n).numel() for n in self.NAMES)
+
+
+def sage3_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: FP4QKV | None = None,
+                       nonfinite: torch.Tensor | None = None, stream=None) -> FP4QKV:
+    """Alg1 L2 + L7 (smoothing K, NVFP4 φ of Q, K, V): see include/sage3.h."""
+    B, H, N, d = q.shape
+    assert k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dtype in (torch.float16, torch.bfloat16)
+    if out is None:
+        out = FP4QKV(B, H, N, d, q.device)
+    flag = ctypes.c_void_p(nonfinite.data_ptr() if nonfinite is not None else None)
+    st = load().sage3_quantize_qkv(_t4(q), _t4(k), _t4(v), _DT[q.dtype], B, H, N, d, ctypes.byref(out.struct),
+                                   ctypes.c_void_p(out.workspace.data_ptr()), out.workspace.numel(), flag,
+                                   _stream(stream))
+    _check(st, "sage3_quantize_qkv")
+    return out
+
+
+def sage3_attn_fwd(qkv: FP4QKV, o: torch.Tensor | None = None, *, causal: bool = False,
+                   softmax_scale: float = 0.0, lse: torch.Tensor | None = None, out_dtype=torch.bfloat16,
+                   stream=None) -> torch.Tensor:
+    """Alg1 L6-L13 (FP4 QK^T, online softmax, two-level P, FP4 PV, O/l): see include/sage3.h."""
+    if o is None:
+        o = torch.empty(qkv.B, qkv.H, qkv.N, qkv.d, dtype=out_dtype, device=qkv.q_data.device)
+    lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
+    st = load().sage3_attn_fwd(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], 1 if causal else 0,
+                               float(softmax_scale), lse_p, _stream(stream))
+    _check(st, "sage3_attn_fwd")
+    return o
+
+
+def sage3_forward_host_scratch_bytes(B, H, N, d, in_dtype=torch.bfloat16, out_dtype=torch.bfloat16) -> int:
+    return int(load().sage3_forward_host_scratch_bytes(B, H, N, d, _DT[in_dtype], _DT[out_dtype]))
+
+
+def sage3_forward_host(q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch.Tensor, o_host: torch.Tensor,
+                       scratch: torch.Tensor, *, causal: bool = False, softmax_scale: float = 0.0, stream=None):
+    """Host-buffer end-to-end path (H2D, quantize, attention, D2H enqueued on `stream`; not synchronized)."""
+    B, H, N, d = q_host.shape
+    for t in (q_host, k_host, v_host, o_host):
+        assert t.device.type == "cpu" and t.is_contiguous()
+    st = load().sage3_forward_host(ctypes.c_void_p(q_host.data_ptr()), ctypes.c_void_p(k_host.data_ptr()),
+                                   ctypes.c_void_p(v_host.data_ptr()), _DT[q_host.dtype], B, H, N, d,
+                                   1 if causal else 0, float(softmax_scale), ctypes.c_void_p(o_host.data_ptr()),
+                                   _DT[o_host.dtype], ctypes.c_void_p(scratch.data_ptr()), scratch.numel(),
+                                   _stream(stream))
+    _check(st, "sage3_forward_host")
+    return o_host
+
+
+def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
+              softmax_scale: float = 0.0, out_dtype=None, stream=None) -> torch.Tensor:
+    """Quantize + attention in one call (the two ABI calls, enqueued on the current stream)."""
+    qkv = sage3_quantize_qkv(q, k, v, stream=stream)
+    return sage3_attn_fwd(qkv, causal=causal, softmax_scale=softmax_scale, out_dtype=out_dtype or q.dtype,
+                          stream=stream)
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,212 @@
+// abi.cu — the extern "C" entry points declared in include/sage3.h: argument validation, size queries,
+// and the launches of quant.cu / attn.cu.  No torch types, no allocation, no synchronization.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/sage3.h"
+#include "internal.h"
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+sage3_status cuda_fail(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return SAGE3_ERR_CUDA;
+}
+
+bool shape_ok(int B, int H, int N, int d) {
+  if (B < 1 || H < 1 || N < 1 || (d != 64 && d != 128)) return false;
+  // 32-bit grid / index limits of the kernels
+  const int64_t Np = ((int64_t)N + 127) / 128 * 128;
+  if ((int64_t)B * H > 65535 || Np / 128 > 65535 || (int64_t)B * H * Np > (int64_t)1 << 31) return false;
+  return true;
+}
+
+int64_t npad(int N) { return ((int64_t)N + 127) / 128 * 128; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// A [B][H][N][d] operand of `esize`-byte elements: non-null, 16-byte aligned base and row/batch/head strides.
+bool tensor_ok(const sage3_tensor4& t, int esize) {
+  if (t.ptr == nullptr || !aligned16(t.ptr)) return false;
+  if ((t.stride_n * esize) % 16 || (t.stride_h * esize) % 16 || (t.stride_b * esize) % 16) return false;
+  return t.stride_n > 0 && t.stride_h >= 0 && t.stride_b >= 0;
+}
+
+sage3_status device_ok() {
+  int dev = 0, major = 0, minor = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? SAGE3_OK : SAGE3_ERR_UNSUPPORTED;
+}
+
+int esize_of(sage3_dtype t) { return t == SAGE3_FP32 ? 4 : 2; }
+
+}  // namespace
+
+extern "C" {
+
+sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]) {
+  if (!bytes || !shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
+  const size_t BH = (size_t)B * H, Np = (size_t)npad(N);
+  bytes[0] = BH * Np * d / 2;   // q_data
+  bytes[1] = BH * Np * d / 2;   // k_data
+  bytes[2] = BH * d * Np / 2;   // v_data
+  bytes[3] = BH * Np * d / 16;  // q_sf
+  bytes[4] = BH * Np * d / 16;  // k_sf
+  bytes[5] = BH * 128 * Np / 16;  // v_sf (128 channel rows, zero beyond d)
+  bytes[6] = BH * d * sizeof(float);  // k_mean
+  return SAGE3_OK;
+}
+
+size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d) {
+  if (!shape_ok(B, H, N, d)) return 0;
+  return (size_t)B * H * (size_t)(npad(N) / 128) * d * sizeof(double);
+}
+
+int sage3_kv_tile(int d) { return (d == 64 || d == 128) ? 128 : 0; }
+
+sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 v, sage3_dtype in_dtype, int B,
+                                int H, int N, int d, sage3_fp4_qkv* out, void* workspace, size_t workspace_bytes,
+                                uint32_t* nonfinite_flag, void* stream) {
+  if (!out || !shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
+  if (in_dtype != SAGE3_FP16 && in_dtype != SAGE3_BF16) return SAGE3_ERR_UNSUPPORTED;
+  if (!tensor_ok(q, 2) || !tensor_ok(k, 2) || !tensor_ok(v, 2)) return SAGE3_ERR_INVALID_ARG;
+  if (out->B != B || out->H != H || out->N != N || out->d != d) return SAGE3_ERR_INVALID_ARG;
+  if (!out->q_data || !out->k_data || !out->v_data || !out->q_sf || !out->k_sf || !out->v_sf || !out->k_mean)
+    return SAGE3_ERR_INVALID_ARG;
+  if (!aligned16(out->q_data) || !aligned16(out->k_data) || !aligned16(out->v_data) || !aligned16(out->q_sf) ||
+      !aligned16(out->k_sf) || !aligned16(out->v_sf) || !aligned16(out->k_mean))
+    return SAGE3_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < sage3_quantize_workspace_bytes(B, H, N, d)) return SAGE3_ERR_WORKSPACE;
+  sage3_status st = device_ok();
+  if (st != SAGE3_OK) return st;
+  out->N_pad = (int32_t)npad(N);
+  sage3::QKArgs qa{};
+  qa.q = q.ptr;
+  qa.k = k.ptr;
+  qa.q_sb = q.stride_b, qa.q_sh = q.stride_h, qa.q_sn = q.stride_n;
+  qa.k_sb = k.stride_b, qa.k_sh = k.stride_h, qa.k_sn = k.stride_n;
+  qa.B = B, qa.H = H, qa.N = N, qa.Np = out->N_pad, qa.d = d;
+  qa.q_data = out->q_data, qa.k_data = out->k_data, qa.q_sf = out->q_sf, qa.k_sf = out->k_sf;
+  qa.k_mean = out->k_mean;
+  qa.nonfinite = nonfinite_flag;
+  sage3::VArgs va{};
+  va.v = v.ptr;
+  va.sb = v.stride_b, va.sh = v.stride_h, va.sn = v.stride_n;
+  va.H = H, va.N = N, va.Np = out->N_pad, va.d = d;
+  va.v_data = out->v_data, va.v_sf = out->v_sf;
+  va.nonfinite = nonfinite_flag;
+  cudaError_t e = sage3::launch_quantize(qa, va, in_dtype == SAGE3_BF16, static_cast<double*>(workspace),
+                                         static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
+}
+
+sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                            float softmax_scale, float* lse, void* stream) {
+  if (!qkv || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
+  if (qkv->N_pad != npad(qkv->N)) return SAGE3_ERR_INVALID_ARG;
+  if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
+  if (!tensor_ok(o, esize_of(o_dtype))) return SAGE3_ERR_INVALID_ARG;
+  if (!qkv->q_data || !qkv->k_data || !qkv->v_data || !qkv->q_sf || !qkv->k_sf || !qkv->v_sf)
+    return SAGE3_ERR_INVALID_ARG;
+  if (!aligned16(qkv->q_data) || !aligned16(qkv->k_data) || !aligned16(qkv->v_data) || !aligned16(qkv->q_sf) ||
+      !aligned16(qkv->k_sf) || !aligned16(qkv->v_sf))
+    return SAGE3_ERR_INVALID_ARG;
+  if (!(std::isfinite(softmax_scale))) return SAGE3_ERR_INVALID_ARG;
+  sage3_status st = device_ok();
+  if (st != SAGE3_OK) return st;
+  sage3::AttnArgs a{};
+  a.q_data = qkv->q_data, a.k_data = qkv->k_data, a.v_data = qkv->v_data;
+  a.q_sf = qkv->q_sf, a.k_sf = qkv->k_sf, a.v_sf = qkv->v_sf;
+  a.o = o.ptr, a.o_sb = o.stride_b, a.o_sh = o.stride_h, a.o_sn = o.stride_n, a.o_dtype = (int)o_dtype;
+  a.lse = lse;
+  a.B = qkv->B, a.H = qkv->H, a.N = qkv->N, a.Np = qkv->N_pad, a.d = qkv->d;
+  a.causal = causal ? 1 : 0;
+  a.scale = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)qkv->d);
+  cudaError_t e = sage3::launch_attention(a, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
+}
+
+// ---------------------------------------------------------------------------------- host e2e path
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t sage3_forward_host_scratch_bytes(int B, int H, int N, int d, sage3_dtype in_dtype, sage3_dtype o_dtype) {
+  size_t sz[7];
+  if (sage3_fp4_qkv_sizes(B, H, N, d, sz) != SAGE3_OK) return 0;
+  const size_t elems = (size_t)B * H * N * d;
+  size_t total = 3 * align256(elems * esize_of(in_dtype)) + align256(elems * esize_of(o_dtype));
+  for (int i = 0; i < 7; ++i) total += align256(sz[i]);
+  total += align256(sage3_quantize_workspace_bytes(B, H, N, d));
+  return total;
+}
+
+sage3_status sage3_forward_host(const void* q_host, const void* k_host, const void* v_host, sage3_dtype in_dtype,
+                                int B, int H, int N, int d, int causal, float softmax_scale, void* o_host,
+                                sage3_dtype o_dtype, void* scratch, size_t scratch_bytes, void* stream) {
+  if (!q_host || !k_host || !v_host || !o_host || !scratch) return SAGE3_ERR_INVALID_ARG;
+  if (!shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
+  if (in_dtype != SAGE3_FP16 && in_dtype != SAGE3_BF16) return SAGE3_ERR_UNSUPPORTED;
+  const size_t need = sage3_forward_host_scratch_bytes(B, H, N, d, in_dtype, o_dtype);
+  if (need == 0) return SAGE3_ERR_UNSUPPORTED;
+  if (scratch_bytes < need) return SAGE3_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t elems = (size_t)B * H * N * d;
+  const size_t in_b = elems * esize_of(in_dtype), o_b = elems * esize_of(o_dtype);
+  uint8_t* p = static_cast<uint8_t*>(scratch);
+  auto take = [&](size_t n) {
+    uint8_t* r = p;
+    p += align256(n);
+    return r;
+  };
+  uint8_t *dq = take(in_b), *dk = take(in_b), *dv = take(in_b), *dout = take(o_b);
+  size_t sz[7];
+  sage3_fp4_qkv_sizes(B, H, N, d, sz);
+  sage3_fp4_qkv f{};
+  f.B = B, f.H = H, f.N = N, f.d = d;
+  f.q_data = take(sz[0]), f.k_data = take(sz[1]), f.v_data = take(sz[2]);
+  f.q_sf = take(sz[3]), f.k_sf = take(sz[4]), f.v_sf = take(sz[5]);
+  f.k_mean = reinterpret_cast<float*>(take(sz[6]));
+  void* ws = take(sage3_quantize_workspace_bytes(B, H, N, d));
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(dq, q_host, in_b, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMemcpyAsync(dk, k_host, in_b, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMemcpyAsync(dv, v_host, in_b, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
+  const int64_t sn = d, sh = (int64_t)N * d, sb = (int64_t)H * N * d;
+  sage3_tensor4 tq{dq, sb, sh, sn}, tk{dk, sb, sh, sn}, tv{dv, sb, sh, sn}, to{dout, sb, sh, sn};
+  sage3_status st = sage3_quantize_qkv(tq, tk, tv, in_dtype, B, H, N, d, &f, ws,
+                                       sage3_quantize_workspace_bytes(B, H, N, d), nullptr, stream);
+  if (st != SAGE3_OK) return st;
+  st = sage3_attn_fwd(&f, to, o_dtype, causal, softmax_scale, nullptr, stream);
+  if (st != SAGE3_OK) return st;
+  if ((e = cudaMemcpyAsync(o_host, dout, o_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e);
+  return SAGE3_OK;
+}
+
+const char* sage3_status_str(sage3_status s) {
+  switch (s) {
+    case SAGE3_OK:
+      return "SAGE3_OK";
+    case SAGE3_ERR_INVALID_ARG:
+      return "SAGE3_ERR_INVALID_ARG";
+    case SAGE3_ERR_UNSUPPORTED:
+      return "SAGE3_ERR_UNSUPPORTED";
+    case SAGE3_ERR_WORKSPACE:
+      return "SAGE3_ERR_WORKSPACE";
+    case SAGE3_ERR_CUDA:
+      return "SAGE3_ERR_CUDA";
+  }
+  return "SAGE3_ERR_UNKNOWN";
+}
+
+int sage3_last_cuda_error(void) { return g_last_cuda_error; }
+
+const char* sage3_version(void) { return "sage3-b200 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// internal.h — host-side launch interfaces between the C ABI (abi.cu) and the kernels (quant.cu,
+// attn.cu).  Not part of the public ABI (include/sage3.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace sage3 {
+
+struct QKArgs {
+  const void* q;
+  const void* k;
+  int64_t q_sb, q_sh, q_sn, k_sb, k_sh, k_sn;
+  int B, H, N, Np, d;
+  uint8_t *q_data, *k_data, *q_sf, *k_sf;
+  float* k_mean;  // written by the K-mean pass, read by quant_qk
+  uint32_t* nonfinite;
+};
+
+struct VArgs {
+  const void* v;
+  int64_t sb, sh, sn;
+  int H, N, Np, d;
+  uint8_t *v_data, *v_sf;
+  uint32_t* nonfinite;
+};
+
+// k_mean is QKArgs::k_mean (non-const alias for the writer).
+cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream);
+
+struct AttnArgs {
+  const uint8_t *q_data, *k_data, *v_data, *q_sf, *k_sf, *v_sf;
+  void* o;
+  int64_t o_sb, o_sh, o_sn;
+  int o_dtype;  // sage3_dtype
+  float* lse;
+  int B, H, N, Np, d;
+  int causal;
+  float scale;  // softmax scale (S units)
+};
+
+// Returns cudaSuccess or the launch / driver error.  `drv_err` receives a CUresult on descriptor failure.
+cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream);
+
+}  // namespace sage3

@@ -1,0 +1,76 @@
+"""CPU checks of the C-ABI library: it loads without a GPU, exports every function include/sage3.h
+declares, and its host-only logic (size queries, argument validation) behaves as documented."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2505_11594_b200 as s3
+from paper_2505_11594_b200 import build as s3build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    s3build.build()
+    return s3.load()
+
+
+def header_functions():
+    txt = open(os.path.join(ROOT, "include", "sage3.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sage3_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_and_binding_agree():
+    assert header_functions() == sorted(s3.ABI_FUNCTIONS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in header_functions():
+        assert hasattr(lib, name), name
+
+
+def test_version_and_status_strings(lib):
+    assert "sm_100a" in s3.version()
+    assert lib.sage3_status_str(0) == b"SAGE3_OK"
+    assert lib.sage3_status_str(3) == b"SAGE3_ERR_WORKSPACE"
+
+
+def test_size_queries(lib):
+    assert s3.sage3_kv_tile(128) == 128 and s3.sage3_kv_tile(64) == 128 and s3.sage3_kv_tile(96) == 0
+    B, H, N, d = 2, 3, 300, 64
+    Np = 384
+    sizes = s3.sage3_fp4_qkv_sizes(B, H, N, d)
+    assert sizes == [B * H * Np * d // 2] * 3 + [B * H * Np * d // 16] * 2 + [B * H * 128 * Np // 16, B * H * d * 4]
+    assert s3.sage3_quantize_workspace_bytes(B, H, N, d) == B * H * (Np // 128) * d * 8
+    with pytest.raises(s3.Sage3Error):
+        s3.sage3_fp4_qkv_sizes(1, 1, 0, 64)
+    with pytest.raises(s3.Sage3Error):
+        s3.sage3_fp4_qkv_sizes(1, 1, 128, 96)
+
+
+def test_invalid_arguments_rejected_before_any_cuda_call(lib):
+    """Null pointers / bad shapes return SAGE3_ERR_INVALID_ARG on the host (no device needed)."""
+    z = s3.Tensor4(None, 0, 0, 0)
+    f = s3.FP4QKVStruct(1, 1, 128, 64, 128)
+    st = lib.sage3_quantize_qkv(z, z, z, s3.SAGE3_BF16, 1, 1, 128, 64, ctypes.byref(f), None, 0, None, None)
+    assert st == s3.SAGE3_ERR_INVALID_ARG
+    st = lib.sage3_attn_fwd(None, z, s3.SAGE3_BF16, 0, 0.0, None, None)
+    assert st == s3.SAGE3_ERR_INVALID_ARG
+    f.N_pad = 128
+    t = s3.Tensor4(16, 0, 0, 64)  # misaligned-free fake pointer, but the qkv buffers are null
+    st = lib.sage3_attn_fwd(ctypes.byref(f), t, s3.SAGE3_BF16, 0, 0.0, None, None)
+    assert st == s3.SAGE3_ERR_INVALID_ARG
+    st = lib.sage3_forward_host(None, None, None, s3.SAGE3_BF16, 1, 1, 128, 64, 0, 0.0, None, s3.SAGE3_BF16, None, 0,
+                                None)
+    assert st == s3.SAGE3_ERR_INVALID_ARG
+
+
+def test_binding_refuses_missing_library(monkeypatch, tmp_path):
+    monkeypatch.setattr(s3, "_lib", None)
+    monkeypatch.setattr(s3, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(s3.Sage3Error):
+        s3.load()
