@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""Benchmark of the SageAttention3 FP4 attention forward hot path on B200 (BASELINE.json metric:
+"FP4 attention fwd TOPS per B200 (d=128, N=1K-32K) and % of dense FP4 peak").
+
+A step = one pass of the whole hot path over one batch of synthetic input:
+sage3_quantize_qkv (K mean, φ of Q, K, Vᵀ) + sage3_attn_fwd (FP4 QKᵀ, online softmax, two-level P,
+FP4 PV, O/l).  Ops = 4·B·H·N²·d (halved for causal), counted per step on every rank.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 32768] [--causal] [--impl reference]
+
+Multi-GPU (torchrun, one process per GPU): the path shards by (b,h) with no data exchange, so every rank
+runs the per-GPU workload on its own heads (weak scaling); the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+FP4_OVER_BF16 = 9.0 / 2.25  # nominal dense FP4 : BF16 tensor ratio (B200_PROFILING.md nominal table)
+FALLBACK_HBM_GBS, FALLBACK_BF16_TFLOPS = 6650.0, 1590.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return j["hbm_gbs"], j["bf16_tflops"], "measured (MEASURED_PEAKS.json)"
+    return FALLBACK_HBM_GBS, FALLBACK_BF16_TFLOPS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def attn_ops(B, H, N, d, causal):
+    ops = 4.0 * B * H * N * N * d
+    return ops / 2 if causal else ops
+
+
+def load_traffic(workload: str):
+    """Per-launch DRAM traffic of the attention kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        j = json.load(open(p))
+        ent = j.get("attn_fwd", {})
+        if ent.get("workload") == workload:
+            return ent.get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+    return None
+
+
+def cpu_baseline(args, d, timeout_s=20.0):
+    """The oracle as it stands (oracle/, plain C fp64 + OpenMP) on a bounded sample of the workload:
+    quantize head 0, then Algorithm 1 for R query rows of it.  TOPS-equivalent = 4·R·N·d / t."""
+    import numpy as np
+
+    import oracle
+
+    N = args.n
+    q, k, v = synth.make_head(N, d, seed=0, b=0, h=0, H=args.heads, dtype=torch.bfloat16, device="cpu")
+    Q, K, V = (x.float().numpy() for x in (q, k, v))
+    nthr = oracle.num_threads()
+    t0 = time.perf_counter()
+    h = oracle.quantize_head(Q, K, V)
+    tq = time.perf_counter() - t0
+    # calibrate on a few rows, then size the sample to ~timeout_s/2 of work
+    rows = np.linspace(0, N - 1, max(nthr, 4)).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.attn_fwd([h], causal=args.causal, scale=1 / math.sqrt(d), rows=rows)
+    t1 = time.perf_counter() - t0
+    R = int(min(max(len(rows), len(rows) * (timeout_s / 2) / max(t1, 1e-3)), N))
+    rows = np.linspace(0, N - 1, R).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.attn_fwd([h], causal=args.causal, scale=1 / math.sqrt(d), rows=rows)
+    ta = time.perf_counter() - t0
+    frac = float(rows.astype(np.float64).mean() + 1) / N if args.causal else 1.0
+    ops = 4.0 * R * N * d * frac
+    return {"value": ops / ta / 1e12, "unit": "TOPS", "cores": nthr, "kind": "oracle",
+            "sample": f"oracle_quantize_head on head 0 ({tq:.2f} s) + Alg1 for {R} evenly spaced query rows of "
+                      f"head 0 at N={N}, d={d} ({ta:.2f} s); TOPS-equivalent = 4*R*N*d/t",
+            "seconds": ta + tq}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed as the reference arm (bounded sample per step)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    d = 128
+    steps = []
+    for _ in range(args.warmup):
+        cpu_baseline(args, d, timeout_s=4.0)
+    for _ in range(args.steps):
+        steps.append(cpu_baseline(args, d, timeout_s=8.0))
+    val = statistics.median(s["value"] for s in steps)
+    cb = dict(steps[-1])
+    cb["value"] = val
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TOPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(s["seconds"] for s in steps) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
+        "data": "synthetic", "config": workload_config(args, d),
+        "cpu_baseline": cb, "e2e": {"value": val, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "FP4 attention fwd TOPS per B200 (d=128, N=1K-32K) and % of dense FP4 peak"
+
+
+def workload_config(args, d):
+    name = f"B=1,H={args.heads},N={args.n},d={d},{'causal' if args.causal else 'non-causal'}"
+    return {"workload": name, "B": 1, "H": args.heads, "N": args.n, "d": d, "causal": bool(args.causal),
+            "per_rank": True, "parallelism": f"heads-sharded x{args.gpus}",
+            "l2": "inputs larger than L2 (3 x %.0f MB bf16 vs 126 MB)" % (args.heads * args.n * d * 2 / 1e6)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--causal", action="store_true")
+    ap.add_argument("--impl", default="sage3", choices=["sage3", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import paper_2505_11594_b200 as s3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    d, B, H, N, causal = 128, 1, args.heads, args.n, args.causal
+    # this rank's heads: global head ids rank*H .. rank*H+H-1 of a (world*H)-head problem (weak scaling)
+    Q = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=dev)
+    K, V = torch.empty_like(Q), torch.empty_like(Q)
+    for i in range(H):
+        Q[0, i], K[0, i], V[0, i] = synth.make_head(N, d, seed=0, b=0, h=rank * H + i, H=H * world,
+                                                    dtype=torch.bfloat16, device=dev)
+    qkv = s3.FP4QKV(B, H, N, d, dev)
+    O = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    n_steps = args.steps
+    ev_q = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_steps)]
+    ev_a = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_steps)]
+
+    def step(i=None):
+        if i is not None:
+            ev_q[i][0].record(stream)
+        s3.sage3_quantize_qkv(Q, K, V, out=qkv, stream=stream)
+        if i is not None:
+            ev_q[i][1].record(stream)
+            ev_a[i][0].record(stream)
+        s3.sage3_attn_fwd(qkv, O, causal=causal, stream=stream)
+        if i is not None:
+            ev_a[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for i in range(n_steps):
+            step(i)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    if dist:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = t.item()
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_step = elapsed_ms / n_steps
+    ops_rank = attn_ops(B, H, N, d, causal)
+    value = ops_rank * world / (ms_step * 1e-3) / 1e12
+    q_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_q)
+    a_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_a)
+
+    hbm_gbs, bf16_tf, peak_src = peaks()
+    fp4_peak = bf16_tf * FP4_OVER_BF16
+    cfg = workload_config(args, d)
+    attn_tflops = ops_rank / (a_ms * 1e-3) / 1e12
+    traffic = load_traffic(cfg["workload"])
+    roofline = {"bound": "tensor", "kernel": "attn_fwd_kernel<128>", "achieved": attn_tflops, "peak": fp4_peak,
+                "unit": "TFLOP/s", "frac": attn_tflops / fp4_peak, "traffic": traffic,
+                "peak_source": f"{peak_src}: bf16_tflops {bf16_tf} x {FP4_OVER_BF16:g} (nominal dense FP4:BF16)",
+                "algorithmic": "4*B*H*N^2*d (x0.5 causal) per launch / mean CUDA-event launch time"}
+    E = B * H * N * d
+    q_bytes = E * (3 * 2) + E * 3 * (0.5 + 1 / 16)  # read Q,K,V bf16; write codes + scales
+    quant = {"ms": q_ms, "algorithmic_bytes": q_bytes, "achieved_GBps": q_bytes / (q_ms * 1e-3) / 1e9,
+             "peak_GBps": hbm_gbs, "frac": q_bytes / (q_ms * 1e-3) / 1e9 / hbm_gbs, "bound": "hbm"}
+
+    # ---- e2e: the same step through the C-ABI host-buffer entry point (H2D + quantize + attn + D2H)
+    e2e = None
+    if not args.no_e2e:
+        qh, kh, vh = (x.cpu().pin_memory() for x in (Q, K, V))
+        oh = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
+        scratch = torch.empty(s3.sage3_forward_host_scratch_bytes(B, H, N, d), dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            s3.sage3_forward_host(qh, kh, vh, oh, scratch, causal=causal, stream=stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        k_e2e = max(3, min(n_steps, 10))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k_e2e):
+            s3.sage3_forward_host(qh, kh, vh, oh, scratch, causal=causal, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": ops_rank * world / (ems / k_e2e * 1e-3) / 1e12, "unit": "TOPS",
+               "ms_per_step": ems / k_e2e, "h2d_bytes_per_step": 3 * E * 2, "d2h_bytes_per_step": E * 2,
+               "api": "sage3_forward_host (pinned host buffers)"}
+        del scratch
+
+    # ---- attention-only sweep over the metric's N range (device-timed, this GPU)
+    sweep = None
+    if not args.no_sweep and rank == 0:
+        sweep = []
+        for n in (1024, 2048, 4096, 8192, 16384, 32768):
+            for c in (False, True):
+                q2, k2, v2 = synth.make_qkv(1, H, n, d, seed=1, dtype=torch.bfloat16, device=dev)
+                f = s3.sage3_quantize_qkv(q2, k2, v2, stream=stream)
+                o2 = torch.empty_like(q2)
+                reps = max(3, int(2e13 / attn_ops(1, H, n, d, c) / 50))
+                for _ in range(3):
+                    s3.sage3_attn_fwd(f, o2, causal=c, stream=stream)
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                for _ in range(reps):
+                    s3.sage3_attn_fwd(f, o2, causal=c, stream=stream)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                ms = a0.elapsed_time(a1) / reps
+                tops = attn_ops(1, H, n, d, c) / (ms * 1e-3) / 1e12
+                sweep.append({"N": n, "causal": c, "attn_ms": round(ms, 4), "attn_TOPS": round(tops, 1),
+                              "pct_fp4_peak": round(100 * tops / fp4_peak, 2)})
+                del q2, k2, v2, f, o2
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args, d)
+            cpu.pop("seconds", None)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "TOPS", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": n_steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "nvfp4 (e2m1 codes, e4m3 1x16 scales), fp32 accumulate; bf16 in/out",
+            "data": "synthetic (seeded Gaussian Q/K/V with outlier channels; synth/)",
+            "config": cfg, "pct_fp4_peak": 100 * value / world / fp4_peak,
+            "breakdown_ms": {"quantize": q_ms, "attention": a_ms},
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": 5 * n_steps, "launches_per_step": 5,
+            "roofline": roofline, "quantize_roofline": quant, "cpu_baseline": cpu, "sweep": sweep,
+            "context": {"paper_RTX5090_TOPS": 1038, "paper_B200_theoretical_TOPS": 10000},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

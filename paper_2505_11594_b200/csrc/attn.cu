@@ -1,24 +1,28 @@
 // attn.cu — sm_100a SageAttention3 FP4 attention forward: Algorithm 1 L6-L13.
 //
 // One CTA = one 128-row query tile Q_i of one (b,h); loop over 128-key tiles j (B_q = B_kv = 128).
-// Warp roles (12 warps, 3 warpgroups):
-//   warp 0      TMA producer: Q̂_i + s_Q once; K̂_j + s_K and V̂ᵀ_j + s_V per stage (kStages ring)
-//   warp 1      MMA issuer (one elected lane):
-//                 S_j  = FP4MM(Q̂_i, s_Q, K̂_j, s_K)        tcgen05.mma kind::mxf4nvf4, M=128 N=128 K=d
-//                 PV_j = FP4MM(P̂2_j, s_P2, V̂_j, s_V)      M=128 N=d K=128, fresh TMEM accumulator
-//               scale factors are staged smem -> TMEM with tcgen05.cp.32x128b.warpx4 in issue order
-//   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   softmax: one query row per thread (TMEM lane = row); online softmax (Alg1 L9) and the
-//               two-level P quantization (Alg1 L10, §3.2) entirely in registers; writes P̂2
-//               (K-major, SWIZZLE_64B) and s_P2 (SF atoms) to smem for the PV MMA
-//   warps 8-11  correction: O kept in registers, O = α·O + s_P1·PV_j (Alg1 L11), O/l (L13), store
+// Warp roles (16 warps, 4 warpgroups, 1 CTA per SM):
+//   WG0 warp 0   TMA producer: Q̂_i + s_Q once; K̂_j + s_K and V̂ᵀ_j + s_V per stage (kStages ring)
+//       warp 1   MMA issuer (one elected lane):
+//                  S_j  = FP4MM(Q̂_i, s_Q, K̂_j, s_K)      tcgen05.mma kind::mxf4nvf4, M=128 N=128 K=d
+//                  PV_j = FP4MM(P̂2_j, s_P2, V̂_j, s_V)    M=128 N=d K=128, fresh TMEM accumulator
+//                scale factors go smem -> TMEM with tcgen05.cp.32x128b.warpx4, in MMA issue order
+//       warp 2   TMEM allocator (512 columns)
+//   WG1, WG2     softmax + two-level P quantization, one query row per thread (TMEM lane = row);
+//                WG1 takes the even KV tiles (S buffer 0), WG2 the odd ones (S buffer 1).  A tile's P̂2
+//                codes and s_P2 depend only on that tile's row max (see below), so the two warpgroups
+//                never synchronise with each other.
+//   WG3          correction: owns the online-softmax recurrence (m, l; Alg1 L9) and O in registers:
+//                O = α·O + s_P1·PV_j (Alg1 L11), then O/l (L13) and the store.
 //
-// Two-level P identity used on the GPU (reading c14): with tmax = rowmax(S_ij) and
-// m_ij = max(m_{i,j-1}, tmax),
-//     P̃2 = P̃ / s_P1 = 2688 · exp(scale·(S − tmax))          (max element = 2688 -> s_P2 = 448, code 6)
-//     s_P1 = rowmax(P̃)/2688 = exp(scale·(tmax − m_ij)) / 2688
-//     l_ij = e^{scale(m_{i,j-1} − m_ij)} l_{i,j-1} + s_P1 · rowsum(P̃2)
-// and exp(x) = 2^(x·log2 e) on MUFU.EX2.
+// Two-level P in tile-local form (reading c14): with tmax_j = rowmax(S_ij),
+// m_j = max(m_{j-1}, tmax_j) and the scale folded into log2 units (sl2 = scale·log2 e):
+//     P̃2_j = P̃_j / s_P1 = 2688 · 2^{sl2 (S − tmax_j)}         (max element = 2688 -> s_P2 = 448, code 6)
+//     s_P1 = rowmax(P̃_j)/2688 = 2^{sl2 (tmax_j − m_j)} / 2688
+//     l_j  = 2^{sl2 (m_{j-1} − m_j)} l_{j-1} + s_P1 · rowsum(P̃2_j)
+// The 16-key block maxima of S are taken once (pass 1) and reused twice (the paper's "reuse" of the
+// block max): their max is tmax_j, and 2688·2^{sl2 (bmax − tmax)} is the block amax of P̃2
+// that sets s_P2 (exp is monotone, and the argmax element is computed by the identical instruction).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -37,7 +41,7 @@ namespace {
 using namespace ptx;
 
 constexpr int kStages = 3;
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr float kOneSixth = 0x1.555556p-3f;  // fl32(1/6)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_2688 = 11.392317422778761f;  // log2(448 * 6)
@@ -48,27 +52,27 @@ constexpr uint32_t kColSFQ = 384, kColSFK = 392, kColSFV = 400, kColSFP = 408;
 
 template <int D>
 struct Layout {
-  static constexpr int kQKRow = D / 2;         // bytes per Q/K row (64 or 32)
-  static constexpr int kQBytes = 128 * kQKRow;  // Q tile codes
+  static constexpr int kQKRow = D / 2;          // bytes per Q/K row (64 or 32)
+  static constexpr int kQBytes = 128 * kQKRow;   // Q tile codes
   static constexpr int kKBytes = 128 * kQKRow;
-  static constexpr int kVBytes = D * 64;     // Vᵀ tile: D channel rows x 128 tokens (64 B)
-  static constexpr int kPBytes = 128 * 64;   // P̂2 tile: 128 rows x 128 keys (64 B)
-  static constexpr int kQKSF = (D / 64) * 512;  // SF atoms per 128-row tile along d
-  static constexpr int kVSF = 1024, kPSF = 1024;  // 8 token-blocks = 2 atoms
+  static constexpr int kKSlot = ((kKBytes + 1023) / 1024) * 1024;
+  static constexpr int kVBytes = D * 64;    // Vᵀ tile: D channel rows x 128 tokens (64 B)
+  static constexpr int kPBytes = 128 * 64;  // P̂2 tile: 128 rows x 128 keys (64 B)
+  static constexpr int kQKSF = (D / 64) * 512;     // SF atoms per 128-row tile along d
+  static constexpr int kVSF = 1024, kPSF = 1024;   // 8 token blocks = 2 atoms
   // byte offsets inside the 1024-aligned dynamic smem window
   static constexpr int oQ = 0;
   static constexpr int oK = oQ + ((kQBytes + 1023) / 1024) * 1024;
-  static constexpr int oV = oK + kStages * ((kKBytes + 1023) / 1024) * 1024;
+  static constexpr int oV = oK + kStages * kKSlot;
   static constexpr int oP = oV + kStages * kVBytes;
   static constexpr int oQSF = oP + 2 * kPBytes;
   static constexpr int oKSF = oQSF + kQKSF;
   static constexpr int oVSF = oKSF + kStages * kQKSF;
   static constexpr int oPSF = oVSF + kStages * kVSF;
-  static constexpr int oXchg = oPSF + 2 * kPSF;       // float [4 slots][2][128]
-  static constexpr int oLut = oXchg + 4 * 2 * 128 * 4;  // float [128] exact 1/s per E4M3 code
-  static constexpr int oFin = oLut + 128 * 4;          // float [2][128] final l, m
-  static constexpr int oBar = oFin + 2 * 128 * 4;      // mbarriers (8 B each)
-  static constexpr int kNumBars = 1 + 4 * kStages + 2 + 2 + 2 + 2 + 2 + 4;
+  static constexpr int oXchg = oPSF + 2 * kPSF;         // float [4 slots][2][128]: tmax_j, rowsum(P̃2_j)
+  static constexpr int oLut = oXchg + 4 * 2 * 128 * 4;  // float [128]: exact 1/s per E4M3 code (0 for s=0)
+  static constexpr int oBar = oLut + 128 * 4;
+  static constexpr int kNumBars = 1 + 4 * kStages + 2 + 2 + 2 + 2 + 4 + 2;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
@@ -80,10 +84,13 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ __forceinline__ void setmaxnreg_dec40() { asm volatile("setmaxnreg.dec.sync.aligned.u32 40;"); }
-__device__ __forceinline__ void setmaxnreg_inc232() { asm volatile("setmaxnreg.inc.sync.aligned.u32 232;"); }
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
 
 // tcgen05.wait::ld that also orders the 32 destination registers (they are "+r" operands).
@@ -98,8 +105,20 @@ __device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  tmem_ld_32x32b_x32(taddr, v);
+  tmem_ld_wait_regs(v);
+}
+
 __device__ __forceinline__ uint64_t sf_desc(const void* p) {
   return make_smem_desc(smem_u32(p), 0, 128, kLayoutNone);
+}
+
+// max of 16 floats as a 3-input tree (FMNMX3)
+__device__ __forceinline__ float max16(const float* v) {
+  const float a = fmax3(v[0], v[1], v[2]), b = fmax3(v[3], v[4], v[5]), c = fmax3(v[6], v[7], v[8]);
+  const float d = fmax3(v[9], v[10], v[11]), e = fmax3(v[12], v[13], v[14]);
+  return fmax3(fmax3(a, b, c), fmax3(d, e, v[15]), -INFINITY);
 }
 
 template <int D>
@@ -114,7 +133,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQSF = smem + L::oQSF;
   float* xchg = reinterpret_cast<float*>(smem + L::oXchg);
   float* lut = reinterpret_cast<float*>(smem + L::oLut);
-  float* fin = reinterpret_cast<float*>(smem + L::oFin);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
@@ -125,9 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_empty = s_full + 2;
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 2;
-  uint64_t* pv_full = p_empty + 2;
+  uint64_t* x_full = p_empty + 2;
+  uint64_t* pv_full = x_full + 4;
   uint64_t* pv_empty = pv_full + 1;
-  uint64_t* x_full = pv_empty + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -150,9 +168,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[b], 128);
       mbar_init(&p_empty[b], 1);
     }
+    for (int s = 0; s < 4; ++s) mbar_init(&x_full[s], 128);
     mbar_init(pv_full, 1);
     mbar_init(pv_empty, 128);
-    for (int s = 0; s < 4; ++s) mbar_init(&x_full[s], 128);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -173,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int wg = warp >> 2;
 
   if (wg == 0) {
-    setmaxnreg_dec40();
+    setmaxnreg_dec<40>();
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer
       if (elect_one()) {
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row_k = bh * a.Np + j * 128;
           mbar_wait(&k_empty[st], ph ^ 1u);
           mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
-          tma_load_2d(smem + L::oK + st * ((L::kKBytes + 1023) / 1024) * 1024, &tm_k, &k_full[st], 0, row_k);
+          tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
           bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)row_k * (D / 16), L::kQKSF, &k_full[st]);
           mbar_wait(&v_empty[st], ph ^ 1u);
           mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&s_empty[b], ((uint32_t)(j >> 1) & 1u) ^ 1u);
           mbar_wait(&k_full[st], (uint32_t)(j / kStages) & 1u);
           tc_fence_after();
-          const uint8_t* sK = smem + L::oK + st * ((L::kKBytes + 1023) / 1024) * 1024;
+          const uint8_t* sK = smem + L::oK + st * L::kKSlot;
           const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
 #pragma unroll
           for (int ks = 0; ks < D / 64; ++ks) tmem_cp_32x128b_x4(tbase + kColSFK + 4 * ks, sf_desc(sKSF + 512 * ks));
@@ -260,152 +278,176 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     }
-  } else if (wg == 1) {
+  } else if (wg <= 2) {
     // -------------------------------------------------------------------- softmax + two-level P quant
-    setmaxnreg_inc232();
-    const int r = threadIdx.x - 128;  // query row in the tile == TMEM lane
+    setmaxnreg_inc<136>();
+    const int par = wg - 1;  // this warpgroup's KV-tile parity == its S / P buffer
+    const int r = threadIdx.x - 128 * wg;  // query row in the tile == TMEM lane
     const int q_row = qt * 128 + r;
-    const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t s_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (par ? kColS1 : kColS0);
     const float sl2 = a.scale * kLog2e;
-    float m = -INFINITY, l = 0.0f;
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (uint32_t)(j >> 1) & 1u);
+    const f2 sl2x2{sl2, sl2};
+    uint8_t* sP = smem + L::oP + par * L::kPBytes;
+    uint8_t* sPSF = smem + L::oPSF + par * L::kPSF;
+    const int sfo = (r & 31) * 16 + (r >> 5) * 4;
+    for (int j = par, it = 0; j < nkv; j += 2, ++it) {
+      mbar_wait(&s_full[par], (uint32_t)it & 1u);
       tc_fence_after();
-      float s[128];
+      const int kv0 = j * 128;
+      const bool masked = kv0 + 128 > a.N || (a.causal && j == qt);
+      const int lim = a.causal ? min(a.N - 1, q_row) - kv0 : a.N - 1 - kv0;  // last visible key in tile
+      // ---- pass 1: 16-key block maxima of S (reused for the row max and for s_P2)
+      float bmax[8];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(lane_addr + (b ? kColS1 : kColS0) + 32 * c, v);
-        tmem_ld_wait_regs(v);
+        tmem_ld32(s_addr + 32 * c, v);
+        float* f = reinterpret_cast<float*>(v);
+        if (masked) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[32 * c + i] = __uint_as_float(v[i]);
+          for (int t = 0; t < 32; ++t)
+            if (32 * c + t > lim) f[t] = -INFINITY;
+        }
+        bmax[2 * c] = max16(f);
+        bmax[2 * c + 1] = max16(f + 16);
+      }
+      const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
+                               fmaxf(bmax[6], bmax[7]));
+      const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb)
+      const f2 nbx2{nb, nb};
+      mbar_wait(&p_empty[par], ((uint32_t)it & 1u) ^ 1u);
+      // ---- pass 2: P̃2, rowsum(P̃2), φ(P̃2) per 16-key block, P̂2 / s_P2 to smem
+      f2 acc0{0.f, 0.f}, acc1{0.f, 0.f};
+      uint32_t scw[2] = {0u, 0u};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(s_addr + 32 * c, v);
+        float* f = reinterpret_cast<float*>(v);
+        if (masked) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (32 * c + t > lim) f[t] = -INFINITY;
+        }
+        float p[32];
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          const f2 x = ffma2(make_float2(f[t], f[t + 1]), sl2x2, nbx2);
+          p[t] = ex2(x.x);
+          p[t + 1] = ex2(x.y);
+        }
+#pragma unroll
+        for (int t = 0; t < 32; t += 4) {
+          acc0 = fadd2(acc0, make_float2(p[t], p[t + 1]));
+          acc1 = fadd2(acc1, make_float2(p[t + 2], p[t + 3]));
+        }
+        uint32_t w[4];
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+          const int blk = 2 * c + hb;
+          const float amax = ex2(fmaf(bmax[blk], sl2, nb));  // == max of the block's P̃2 values
+          const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
+          const float rcp = lut[sc];
+          const f2 rr{rcp, rcp};
+          f2 y[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) y[i] = fmul2(make_float2(p[16 * hb + 2 * i], p[16 * hb + 2 * i + 1]), rr);
+          w[2 * hb] = cvt_e2m1x8(y[0].x, y[0].y, y[1].x, y[1].y, y[2].x, y[2].y, y[3].x, y[3].y);
+          w[2 * hb + 1] = cvt_e2m1x8(y[4].x, y[4].y, y[5].x, y[5].y, y[6].x, y[6].y, y[7].x, y[7].y);
+          scw[blk >> 2] |= sc << (8 * (blk & 3));
+        }
+        // 16-byte chunk c = keys [32c, 32c+32) of row r, SWIZZLE_64B (chunk ^= (row>>1)&3)
+        *reinterpret_cast<uint4*>(sP + r * 64 + ((c ^ ((r >> 1) & 3)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       tc_fence_before();
-      mbar_arrive(&s_empty[b]);
-      const int kv0 = j * 128;
-      if (kv0 + 128 > a.N || (a.causal && j == qt)) {
-        const int lim = a.causal ? min(a.N - 1, q_row) : a.N - 1;
-#pragma unroll
-        for (int t = 0; t < 128; ++t)
-          if (kv0 + t > lim) s[t] = -INFINITY;
-      }
-      float tmax = s[0];
-#pragma unroll
-      for (int t = 1; t < 128; ++t) tmax = fmaxf(tmax, s[t]);
-      const float m_new = fmaxf(m, tmax);
-      const float alpha = ex2((m - m_new) * sl2);
-      const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb) = 2688·e^{scale(S − tmax)}
-      float rowsum = 0.0f;
-#pragma unroll
-      for (int t = 0; t < 128; ++t) {
-        s[t] = ex2(fmaf(s[t], sl2, nb));
-        rowsum += s[t];
-      }
-      const float sP1 = ex2((tmax - m_new) * sl2 - kLog2_2688);
-      l = alpha * l + sP1 * rowsum;
-      // φ(P̃2) over 8 blocks of 16 keys (Eq. 1 with readings c2-c5)
-      uint32_t packed[16];
-      uint32_t scw0 = 0, scw1 = 0;
-#pragma unroll
-      for (int blk = 0; blk < 8; ++blk) {
-        float amax = s[16 * blk];
-#pragma unroll
-        for (int i = 1; i < 16; ++i) amax = fmaxf(amax, s[16 * blk + i]);
-        const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
-        const float rcp = lut[sc];
-        uint32_t bytes[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          bytes[i] = cvt_e2m1x2(__fmul_rn(s[16 * blk + 2 * i], rcp), __fmul_rn(s[16 * blk + 2 * i + 1], rcp));
-        packed[2 * blk] = bytes[0] | (bytes[1] << 8) | (bytes[2] << 16) | (bytes[3] << 24);
-        packed[2 * blk + 1] = bytes[4] | (bytes[5] << 8) | (bytes[6] << 16) | (bytes[7] << 24);
-        if (blk < 4)
-          scw0 |= sc << (8 * blk);
-        else
-          scw1 |= sc << (8 * (blk - 4));
-      }
-      const int pb = j & 1;
-      mbar_wait(&p_empty[pb], ((uint32_t)(j >> 1) & 1u) ^ 1u);
-      uint8_t* sP = smem + L::oP + pb * L::kPBytes;
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {  // 16-byte chunk ch = keys [32ch, 32ch+32), SWIZZLE_64B
-        const int phys = ch ^ ((r >> 1) & 3);
-        *reinterpret_cast<uint4*>(sP + r * 64 + phys * 16) =
-            make_uint4(packed[4 * ch], packed[4 * ch + 1], packed[4 * ch + 2], packed[4 * ch + 3]);
-      }
-      uint8_t* sPSF = smem + L::oPSF + pb * L::kPSF;
-      const int sfo = (r & 31) * 16 + (r >> 5) * 4;
-      *reinterpret_cast<uint32_t*>(sPSF + sfo) = scw0;
-      *reinterpret_cast<uint32_t*>(sPSF + 512 + sfo) = scw1;
+      mbar_arrive(&s_empty[par]);
+      *reinterpret_cast<uint32_t*>(sPSF + sfo) = scw[0];
+      *reinterpret_cast<uint32_t*>(sPSF + 512 + sfo) = scw[1];
+      const f2 acc = fadd2(acc0, acc1);
       const int slot = j & 3;
-      xchg[slot * 256 + r] = alpha;
-      xchg[slot * 256 + 128 + r] = sP1;
+      xchg[slot * 256 + r] = tmax;
+      xchg[slot * 256 + 128 + r] = acc.x + acc.y;
       fence_proxy_async_smem();
-      mbar_arrive(&p_full[pb]);
+      mbar_arrive(&p_full[par]);
       mbar_arrive(&x_full[slot]);
-      m = m_new;
     }
-    fin[r] = l;
-    fin[128 + r] = m;
-    if (a.lse != nullptr && q_row < a.N) a.lse[(int64_t)bh * a.N + q_row] = m * a.scale + logf(l);
-    named_bar_sync(1, 256);
   } else {
     // -------------------------------------------------------------------- correction + epilogue
-    setmaxnreg_inc232();
-    const int r = threadIdx.x - 256;
+    setmaxnreg_inc<200>();
+    const int r = threadIdx.x - 384;
     const int q_row = qt * 128 + r;
-    const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-    float o[D];
+    const uint32_t pv_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16) + kColPV;
+    const float sl2 = a.scale * kLog2e;
+    float m = -INFINITY, l = 0.0f;
+    f2 o[D / 2];
 #pragma unroll
-    for (int c = 0; c < D; ++c) o[c] = 0.0f;
+    for (int c = 0; c < D / 2; ++c) o[c] = make_float2(0.f, 0.f);
     for (int j = 0; j < nkv; ++j) {
       const int slot = j & 3;
       mbar_wait(&x_full[slot], (uint32_t)(j >> 2) & 1u);
-      const float alpha = xchg[slot * 256 + r];
-      const float sP1 = xchg[slot * 256 + 128 + r];
+      const float tmax = xchg[slot * 256 + r];
+      const float rs2 = xchg[slot * 256 + 128 + r];
+      // Alg1 L9: m_ij = max(m_{i,j-1}, rowmax S_ij); l_ij = e^{m_old − m_new} l + rowsum(P̃_ij)
+      const float m_new = fmaxf(m, tmax);
+      const float alpha = ex2((m - m_new) * sl2);
+      const float sP1 = ex2((tmax - m_new) * sl2 - kLog2_2688);  // s_P1 = rowmax(P̃_ij) / 2688
+      l = fmaf(alpha, l, sP1 * rs2);
+      m = m_new;
+      // Alg1 L11: O = diag(α) O + FP4MM(P̂2, s_P2, V̂, s_V) · s_P1
       mbar_wait(pv_full, (uint32_t)j & 1u);
       tc_fence_after();
+      const f2 aa{alpha, alpha}, ss{sP1, sP1};
+      const bool no_rescale = __all_sync(0xffffffffu, alpha == 1.0f);
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(lane_addr + kColPV + 32 * c, v);
-        tmem_ld_wait_regs(v);
+        tmem_ld32(pv_addr + 32 * c, v);
+        if (no_rescale) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[32 * c + i] = fmaf(alpha, o[32 * c + i], sP1 * __uint_as_float(v[i]));
+          for (int i = 0; i < 16; ++i)
+            o[16 * c + i] = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), ss, o[16 * c + i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            o[16 * c + i] =
+                ffma2(aa, o[16 * c + i], fmul2(ss, make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]))));
+        }
       }
       tc_fence_before();
       mbar_arrive(pv_empty);
     }
-    named_bar_sync(1, 256);
-    const float inv_l = 1.0f / fin[r];
+    // Alg1 L13: O_i = diag(l)^-1 O_i
+    if (a.lse != nullptr && q_row < a.N) a.lse[(int64_t)bh * a.N + q_row] = m * a.scale + logf(l);
+    const float inv_l = 1.0f / l;
     if (q_row < a.N) {
       const int b = bh / a.H, h = bh % a.H;
+      const f2 il{inv_l, inv_l};
+#pragma unroll
+      for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
       if (a.o_dtype == 2) {
         float* dst = reinterpret_cast<float*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
 #pragma unroll
-        for (int c = 0; c < D; c += 4)
-          *reinterpret_cast<float4*>(dst + c) =
-              make_float4(o[c] * inv_l, o[c + 1] * inv_l, o[c + 2] * inv_l, o[c + 3] * inv_l);
+        for (int c = 0; c < D / 2; c += 2)
+          *reinterpret_cast<float4*>(dst + 2 * c) = make_float4(o[c].x, o[c].y, o[c + 1].x, o[c + 1].y);
       } else if (a.o_dtype == 1) {
         __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
 #pragma unroll
-        for (int c = 0; c < D; c += 8) {
+        for (int c = 0; c < D / 2; c += 4) {
           uint4 u;
           __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
-          *reinterpret_cast<uint4*>(dst + c) = u;
+          for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(o[c + i].x, o[c + i].y);
+          *reinterpret_cast<uint4*>(dst + 2 * c) = u;
         }
       } else {
         __half* dst = reinterpret_cast<__half*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
 #pragma unroll
-        for (int c = 0; c < D; c += 8) {
+        for (int c = 0; c < D / 2; c += 4) {
           uint4 u;
           __half2* p = reinterpret_cast<__half2*>(&u);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) p[i] = __floats2half2_rn(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
-          *reinterpret_cast<uint4*>(dst + c) = u;
+          for (int i = 0; i < 4; ++i) p[i] = __floats2half2_rn(o[c + i].x, o[c + i].y);
+          *reinterpret_cast<uint4*>(dst + 2 * c) = u;
         }
       }
     }
