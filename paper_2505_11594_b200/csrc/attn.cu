@@ -2,10 +2,11 @@
 //
 // One CTA = one 128-row query tile Q_i of one (b,h); loop over 128-key tiles j (B_q = B_kv = 128).
 // Warp roles (16 warps, 4 warpgroups, 1 CTA per SM):
-//   WG0 warp 0   TMA producer: Q̂_i + s_Q once; K̂_j + s_K and V̂ᵀ_j + s_V per stage (kStages ring)
+//   WG0 warp 0   TMA producer of Q̂_i + s_Q (once) and K̂_j + s_K (kKStages ring)
+//       warp 3   TMA producer of V̂ᵀ_j + s_V (kVStages ring)
 //       warp 1   MMA issuer (one elected lane):
 //                  S_j  = FP4MM(Q̂_i, s_Q, K̂_j, s_K)      tcgen05.mma kind::mxf4nvf4, M=128 N=128 K=d
-//                  PV_j = FP4MM(P̂2_j, s_P2, V̂_j, s_V)    M=128 N=d K=128, fresh TMEM accumulator
+//                  PV_j = FP4MM(P̂2_j, s_P2, V̂_j, s_V)    M=128 N=d K=128, written over S_j's TMEM columns
 //                scale factors go smem -> TMEM with tcgen05.cp.32x128b.warpx4, in MMA issue order
 //       warp 2   TMEM allocator (512 columns)
 //   WG1, WG2     softmax + two-level P quantization, one query row per thread (TMEM lane = row);
@@ -40,14 +41,18 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kStages = 3;
+constexpr int kKStages = 5, kVStages = 4;
+constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
+constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
 constexpr int kThreads = 512;
 constexpr float kOneSixth = 0x1.555556p-3f;  // fl32(1/6)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_2688 = 11.392317422778761f;  // log2(448 * 6)
 
-// TMEM column map (512 columns allocated).
-constexpr uint32_t kColS0 = 0, kColS1 = 128, kColPV = 256;
+// TMEM column map (512 columns allocated): three 128-column buffers; tile j uses buffer j % 3 first for
+// S_j (MMA), then — once the softmax has read S_j — for PV_j (MMA), which the correction warpgroup reads
+// before the buffer is reused for S_{j+3}.  Scale factors in 32 more columns.
+constexpr int kSBufs = 3;
 constexpr uint32_t kColSFQ = 384, kColSFK = 392, kColSFV = 400, kColSFP = 408;
 
 template <int D>
@@ -63,16 +68,16 @@ struct Layout {
   // byte offsets inside the 1024-aligned dynamic smem window
   static constexpr int oQ = 0;
   static constexpr int oK = oQ + ((kQBytes + 1023) / 1024) * 1024;
-  static constexpr int oV = oK + kStages * kKSlot;
-  static constexpr int oP = oV + kStages * kVBytes;
-  static constexpr int oQSF = oP + 2 * kPBytes;
+  static constexpr int oV = oK + kKStages * kKSlot;
+  static constexpr int oP = oV + kVStages * kVBytes;
+  static constexpr int oQSF = oP + kPBufs * kPBytes;
   static constexpr int oKSF = oQSF + kQKSF;
-  static constexpr int oVSF = oKSF + kStages * kQKSF;
-  static constexpr int oPSF = oVSF + kStages * kVSF;
-  static constexpr int oXchg = oPSF + 2 * kPSF;         // float [4 slots][2][128]: tmax_j, rowsum(P̃2_j)
-  static constexpr int oLut = oXchg + 4 * 2 * 128 * 4;  // float [128]: exact 1/s per E4M3 code (0 for s=0)
+  static constexpr int oVSF = oKSF + kKStages * kQKSF;
+  static constexpr int oPSF = oVSF + kVStages * kVSF;
+  static constexpr int oXchg = oPSF + kPBufs * kPSF;            // float [kXSlots][2][128]: tmax_j, rowsum(P̃2_j)
+  static constexpr int oLut = oXchg + kXSlots * 2 * 128 * 4;  // float [128]: exact 1/s per E4M3 code (0 for s=0)
   static constexpr int oBar = oLut + 128 * 4;
-  static constexpr int kNumBars = 1 + 4 * kStages + 2 + 2 + 2 + 2 + 4 + 2;
+  static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + kXSlots;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
@@ -105,6 +110,19 @@ __device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  tmem_ld_32x32b_x16(taddr, v);
+  tmem_ld_wait_regs(v);
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   tmem_ld_32x32b_x32(taddr, v);
   tmem_ld_wait_regs(v);
@@ -131,46 +149,46 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   uint8_t* sQ = smem + L::oQ;
   uint8_t* sQSF = smem + L::oQSF;
-  float* xchg = reinterpret_cast<float*>(smem + L::oXchg);
-  float* lut = reinterpret_cast<float*>(smem + L::oLut);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + kStages;
-  uint64_t* v_full = k_empty + kStages;
-  uint64_t* v_empty = v_full + kStages;
-  uint64_t* s_full = v_empty + kStages;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* p_empty = p_full + 2;
-  uint64_t* x_full = p_empty + 2;
-  uint64_t* pv_full = x_full + 4;
-  uint64_t* pv_empty = pv_full + 1;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + kKStages;
+  uint64_t* v_full = k_empty + kKStages;
+  uint64_t* v_empty = v_full + kVStages;
+  uint64_t* s_full = v_empty + kVStages;  // MMA -> softmax: S_j in buffer j%3
+  uint64_t* pv_full = s_full + kSBufs;    // MMA -> correction: PV_j in buffer j%3
+  uint64_t* b_empty = pv_full + kSBufs;   // correction -> MMA: buffer j%3 free again
+  uint64_t* p_full = b_empty + kSBufs;    // softmax -> MMA: P̂2_j / s_P2 in smem buffer j%4, S_j consumed
+  uint64_t* p_empty = p_full + kPBufs;    // MMA -> softmax: PV_j done with smem buffer j%4
+  uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = a.Np >> 7;
-  const int bh = blockIdx.x;
-  const int qt = n_qt - 1 - (int)blockIdx.y;  // longest-first under causal masking
+  const int qt = n_qt - 1 - (int)blockIdx.x;  // q tiles fastest (CTAs of one head share K/V in L2),
+  const int bh = blockIdx.y;                  // longest-first under causal masking
   const int nkv = a.causal ? qt + 1 : n_qt;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kKStages; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kVStages; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kSBufs; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 128);
+      mbar_init(&pv_full[b], 1);
+      mbar_init(&b_empty[b], 128);
+    }
+    for (int b = 0; b < kPBufs; ++b) {
       mbar_init(&p_full[b], 128);
       mbar_init(&p_empty[b], 1);
     }
-    for (int s = 0; s < 4; ++s) mbar_init(&x_full[s], 128);
-    mbar_init(pv_full, 1);
-    mbar_init(pv_empty, 128);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 128);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -182,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x >= 128 && threadIdx.x < 256) {  // exact reciprocal of every E4M3 scale; 0 for s = 0
     const int c = threadIdx.x - 128;
     const float s = e4m3_to_f32((uint32_t)c);
-    lut[c] = (s == 0.0f || c == 0x7F) ? 0.0f : __frcp_rn(s);
+    reinterpret_cast<float*>(smem + L::oLut)[c] = (s == 0.0f || c == 0x7F) ? 0.0f : __frcp_rn(s);
   }
   tc_fence_before();
   __syncthreads();
@@ -193,21 +211,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (wg == 0) {
     setmaxnreg_dec<40>();
     if (warp == 0) {
-      // ------------------------------------------------------------------ TMA producer
+      // ------------------------------------------------------------------ TMA producer: Q, K
       if (elect_one()) {
         const int row_q = bh * a.Np + qt * 128;
         mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
         tma_load_2d(sQ, &tm_q, q_full, 0, row_q);
         bulk_load(sQSF, a.q_sf + (int64_t)row_q * (D / 16), L::kQKSF, q_full);
         for (int j = 0; j < nkv; ++j) {
-          const int st = j % kStages;
-          const uint32_t ph = (uint32_t)(j / kStages) & 1u;
+          const int st = j % kKStages;
           const int row_k = bh * a.Np + j * 128;
-          mbar_wait(&k_empty[st], ph ^ 1u);
+          mbar_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
           tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
           bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)row_k * (D / 16), L::kQKSF, &k_full[st]);
-          mbar_wait(&v_empty[st], ph ^ 1u);
+        }
+      }
+      __syncwarp();
+    } else if (warp == 3) {
+      // ------------------------------------------------------------------ TMA producer: V
+      if (elect_one()) {
+        for (int j = 0; j < nkv; ++j) {
+          const int st = j % kVStages;
+          mbar_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
           tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
           bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + (int64_t)bh * 128 * (a.Np / 16) + j * 1024, L::kVSF,
@@ -226,9 +251,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < D / 64; ++ks) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * ks, sf_desc(sQSF + 512 * ks));
         auto issue_s = [&](int j) {
-          const int b = j & 1, st = j % kStages;
-          mbar_wait(&s_empty[b], ((uint32_t)(j >> 1) & 1u) ^ 1u);
-          mbar_wait(&k_full[st], (uint32_t)(j / kStages) & 1u);
+          const int b = j % kSBufs, st = j % kKStages;
+          mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
+          mbar_wait(&k_full[st], (uint32_t)(j / kKStages) & 1u);
           tc_fence_after();
           const uint8_t* sK = smem + L::oK + st * L::kKSlot;
           const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
@@ -238,17 +263,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < D / 64; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sQ) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
             const uint64_t bd = make_smem_desc(smem_u32(sK) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
-            mma_nvf4(tbase + (b ? kColS1 : kColS0), ad, bd, idesc_s, tbase + kColSFQ + 4 * ks,
-                     tbase + kColSFK + 4 * ks, ks > 0);
+            mma_nvf4(tbase + 128 * b, ad, bd, idesc_s, tbase + kColSFQ + 4 * ks, tbase + kColSFK + 4 * ks, ks > 0);
           }
           mma_commit(&k_empty[st]);
           mma_commit(&s_full[b]);
         };
         auto issue_pv = [&](int j) {
-          const int pb = j & 1, st = j % kStages;
-          mbar_wait(&p_full[pb], (uint32_t)(j >> 1) & 1u);
-          mbar_wait(&v_full[st], (uint32_t)(j / kStages) & 1u);
-          mbar_wait(pv_empty, ((uint32_t)j & 1u) ^ 1u);
+          const int b = j % kSBufs, pb = j % kPBufs, st = j % kVStages;
+          mbar_wait(&p_full[pb], (uint32_t)(j / kPBufs) & 1u);
+          mbar_wait(&v_full[st], (uint32_t)(j / kVStages) & 1u);
           tc_fence_after();
           const uint8_t* sP = smem + L::oP + pb * L::kPBytes;
           const uint8_t* sV = smem + L::oV + st * L::kVBytes;
@@ -263,16 +286,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < 2; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sP) + 32 * ks, 16, 512, kLayoutSw64);
             const uint64_t bd = make_smem_desc(smem_u32(sV) + 32 * ks, 16, 512, kLayoutSw64);
-            mma_nvf4(tbase + kColPV, ad, bd, idesc_pv, tbase + kColSFP + 4 * ks, tbase + kColSFV + 4 * ks, ks > 0);
+            mma_nvf4(tbase + 128 * b, ad, bd, idesc_pv, tbase + kColSFP + 4 * ks, tbase + kColSFV + 4 * ks, ks > 0);
           }
           mma_commit(&v_empty[st]);
           mma_commit(&p_empty[pb]);
-          mma_commit(pv_full);
+          mma_commit(&pv_full[b]);
         };
         issue_s(0);
         if (nkv > 1) issue_s(1);
         for (int j = 0; j < nkv; ++j) {
-          if (j + 2 < nkv) issue_s(j + 2);
+          if (j + 2 < nkv) issue_s(j + 2);  // buffer (j+2)%3 held PV_{j-1}; freed by the correction
           issue_pv(j);
         }
       }
@@ -281,17 +304,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (wg <= 2) {
     // -------------------------------------------------------------------- softmax + two-level P quant
     setmaxnreg_inc<136>();
-    const int par = wg - 1;  // this warpgroup's KV-tile parity == its S / P buffer
-    const int r = threadIdx.x - 128 * wg;  // query row in the tile == TMEM lane
+    const int par = wg - 1;                 // this warpgroup's KV-tile parity
+    const int r = threadIdx.x - 128 * wg;   // query row in the tile == TMEM lane
     const int q_row = qt * 128 + r;
-    const uint32_t s_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (par ? kColS1 : kColS0);
+    const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t lut_s = smem_u32(smem + L::oLut);
     const float sl2 = a.scale * kLog2e;
-    const f2 sl2x2{sl2, sl2};
-    uint8_t* sP = smem + L::oP + par * L::kPBytes;
-    uint8_t* sPSF = smem + L::oPSF + par * L::kPSF;
-    const int sfo = (r & 31) * 16 + (r >> 5) * 4;
-    for (int j = par, it = 0; j < nkv; j += 2, ++it) {
-      mbar_wait(&s_full[par], (uint32_t)it & 1u);
+    const f2 sl2x2 = make_float2(sl2, sl2);
+    const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
+    for (int j = par; j < nkv; j += 2) {
+      const int sb = j % kSBufs, pb = j % kPBufs;
+      const uint32_t s_addr = lane_base + 128 * sb;
+      const uint32_t sP = smem_u32(smem + L::oP + pb * L::kPBytes) + r * 64;
+      const uint32_t sPSF = smem_u32(smem + L::oPSF + pb * L::kPSF) + (r & 31) * 16 + (r >> 5) * 4;
+      mbar_wait(&s_full[sb], (uint32_t)(j / kSBufs) & 1u);
       tc_fence_after();
       const int kv0 = j * 128;
       const bool masked = kv0 + 128 > a.N || (a.causal && j == qt);
@@ -314,10 +340,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
       const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb)
-      const f2 nbx2{nb, nb};
-      mbar_wait(&p_empty[par], ((uint32_t)it & 1u) ^ 1u);
+      const f2 nbx2 = make_float2(nb, nb);
+      mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
       // ---- pass 2: P̃2, rowsum(P̃2), φ(P̃2) per 16-key block, P̂2 / s_P2 to smem
-      f2 acc0{0.f, 0.f}, acc1{0.f, 0.f};
+      f2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
       uint32_t scw[2] = {0u, 0u};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -347,8 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int blk = 2 * c + hb;
           const float amax = ex2(fmaf(bmax[blk], sl2, nb));  // == max of the block's P̃2 values
           const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
-          const float rcp = lut[sc];
-          const f2 rr{rcp, rcp};
+          const float rcp = lds_f32(lut_s + 4 * sc);
+          const f2 rr = make_float2(rcp, rcp);
           f2 y[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) y[i] = fmul2(make_float2(p[16 * hb + 2 * i], p[16 * hb + 2 * i + 1]), rr);
@@ -357,65 +383,67 @@ __global__ void __launch_bounds__(kThreads, 1)
           scw[blk >> 2] |= sc << (8 * (blk & 3));
         }
         // 16-byte chunk c = keys [32c, 32c+32) of row r, SWIZZLE_64B (chunk ^= (row>>1)&3)
-        *reinterpret_cast<uint4*>(sP + r * 64 + ((c ^ ((r >> 1) & 3)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
       }
-      tc_fence_before();
-      mbar_arrive(&s_empty[par]);
-      *reinterpret_cast<uint32_t*>(sPSF + sfo) = scw[0];
-      *reinterpret_cast<uint32_t*>(sPSF + 512 + sfo) = scw[1];
+      sts_u32(sPSF, scw[0]);
+      sts_u32(sPSF + 512, scw[1]);
       const f2 acc = fadd2(acc0, acc1);
-      const int slot = j & 3;
-      xchg[slot * 256 + r] = tmax;
-      xchg[slot * 256 + 128 + r] = acc.x + acc.y;
+      const int slot = j % kXSlots;
+      sts_f32(xchg_s + slot * 1024, tmax);
+      sts_f32(xchg_s + slot * 1024 + 512, acc.x + acc.y);
+      tc_fence_before();
       fence_proxy_async_smem();
-      mbar_arrive(&p_full[par]);
+      mbar_arrive(&p_full[pb]);
       mbar_arrive(&x_full[slot]);
     }
   } else {
     // -------------------------------------------------------------------- correction + epilogue
+    // O and l are kept relative to a per-row reference max mref (lazily moved: only when a tile max
+    // exceeds it by more than 2^8 in weight), so tile j enters with weight
+    //   w_j = 2^{sl2 (tmax_j − mref)} / 2688  (= s_P1 · Π α relative to mref)
+    // which is Alg1 L9-L11 up to fp32 rounding: O/l and lse are independent of the reference.
     setmaxnreg_inc<200>();
     const int r = threadIdx.x - 384;
     const int q_row = qt * 128 + r;
-    const uint32_t pv_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16) + kColPV;
+    const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
     const float sl2 = a.scale * kLog2e;
-    float m = -INFINITY, l = 0.0f;
+    float mref = -INFINITY, l = 0.0f;
     f2 o[D / 2];
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) o[c] = make_float2(0.f, 0.f);
     for (int j = 0; j < nkv; ++j) {
-      const int slot = j & 3;
-      mbar_wait(&x_full[slot], (uint32_t)(j >> 2) & 1u);
-      const float tmax = xchg[slot * 256 + r];
-      const float rs2 = xchg[slot * 256 + 128 + r];
-      // Alg1 L9: m_ij = max(m_{i,j-1}, rowmax S_ij); l_ij = e^{m_old − m_new} l + rowsum(P̃_ij)
-      const float m_new = fmaxf(m, tmax);
-      const float alpha = ex2((m - m_new) * sl2);
-      const float sP1 = ex2((tmax - m_new) * sl2 - kLog2_2688);  // s_P1 = rowmax(P̃_ij) / 2688
-      l = fmaf(alpha, l, sP1 * rs2);
-      m = m_new;
-      // Alg1 L11: O = diag(α) O + FP4MM(P̂2, s_P2, V̂, s_V) · s_P1
-      mbar_wait(pv_full, (uint32_t)j & 1u);
+      const int slot = j % kXSlots, b = j % kSBufs;
+      mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
+      const float tmax = lds_f32(xchg_s + slot * 1024);
+      const float rs2 = lds_f32(xchg_s + slot * 1024 + 512);
+      const bool need = (tmax - mref) * sl2 > 8.0f;  // true on the first tile (mref = -inf)
+      if (__any_sync(0xffffffffu, need)) {
+        const float mnew = need ? tmax : mref;
+        const float sc = ex2((mref - mnew) * sl2);  // 0 on the first tile, 1 for rows that keep mref
+        const f2 sc2 = make_float2(sc, sc);
+        l *= sc;
+#pragma unroll
+        for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], sc2);
+        mref = mnew;
+      }
+      const float w = ex2((tmax - mref) * sl2 - kLog2_2688);
+      l = fmaf(w, rs2, l);
+      const f2 ww = make_float2(w, w);
+      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
       tc_fence_after();
-      const f2 aa{alpha, alpha}, ss{sP1, sP1};
-      const bool no_rescale = __all_sync(0xffffffffu, alpha == 1.0f);
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(pv_addr + 32 * c, v);
-        if (no_rescale) {
+      for (int c = 0; c < D / 16; ++c) {
+        uint32_t v[16];
+        tmem_ld16(lane_base + 128 * b + 16 * c, v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            o[16 * c + i] = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), ss, o[16 * c + i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            o[16 * c + i] =
-                ffma2(aa, o[16 * c + i], fmul2(ss, make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]))));
-        }
+        for (int i = 0; i < 8; ++i)
+          o[8 * c + i] = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), ww, o[8 * c + i]);
       }
       tc_fence_before();
-      mbar_arrive(pv_empty);
+      mbar_arrive(&b_empty[b]);
     }
+    const float m = mref;
     // Alg1 L13: O_i = diag(l)^-1 O_i
     if (a.lse != nullptr && q_row < a.N) a.lse[(int64_t)bh * a.N + q_row] = m * a.scale + logf(l);
     const float inv_l = 1.0f / l;
@@ -507,7 +535,7 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
       !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
       !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D))
     return cudaErrorInvalidValue;
-  dim3 grid(BH, a.Np / 128);
+  dim3 grid(a.Np / 128, BH);
   attn_fwd_kernel<D><<<grid, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
   return cudaGetLastError();
 }
