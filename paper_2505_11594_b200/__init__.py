@@ -14,7 +14,7 @@ import os
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsage3.so")
+LIB_PATH = os.environ.get("SAGE3_LIB") or os.path.join(PKG, "libsage3.so")  # env override: experiments only
 
 SAGE3_OK, SAGE3_ERR_INVALID_ARG, SAGE3_ERR_UNSUPPORTED, SAGE3_ERR_WORKSPACE, SAGE3_ERR_CUDA = range(5)
 SAGE3_FP16, SAGE3_BF16, SAGE3_FP32 = 0, 1, 2

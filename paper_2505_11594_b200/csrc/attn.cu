@@ -44,6 +44,10 @@ using namespace ptx;
 constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
+#ifndef SAGE3_POLY_PAIRS_PER4
+#define SAGE3_POLY_PAIRS_PER4 1
+#endif
+constexpr int kPolyPairsPer4 = SAGE3_POLY_PAIRS_PER4;  // of every 4 exp2 pairs in pass 2, this many use the polynomial
 constexpr int kThreads = 512;
 constexpr float kOneSixth = 0x1.555556p-3f;  // fl32(1/6)
 constexpr float kLog2e = 1.4426950408889634f;
@@ -75,8 +79,8 @@ struct Layout {
   static constexpr int oVSF = oKSF + kKStages * kQKSF;
   static constexpr int oPSF = oVSF + kVStages * kVSF;
   static constexpr int oXchg = oPSF + kPBufs * kPSF;            // float [kXSlots][2][128]: tmax_j, rowsum(P̃2_j)
-  static constexpr int oLut = oXchg + kXSlots * 2 * 128 * 4;  // float [128]: exact 1/s per E4M3 code (0 for s=0)
-  static constexpr int oBar = oLut + 128 * 4;
+  static constexpr int oLut = oXchg + kXSlots * 2 * 128 * 4;  // float [2][128]: -log2(s), s per E4M3 code
+  static constexpr int oBar = oLut + 2 * 128 * 4;
   static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + kXSlots;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
@@ -87,6 +91,27 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x for a pair on the FMA pipe (offloads MUFU): x = j + f with j = rint(x), f in [-0.5, 0.5];
+// 2^f by a degree-5 fp32 minimax polynomial (max rel. error 2.3e-7, MUFU grade), 2^j added to the
+// exponent field.  x is clamped to >= -126 so the integer add cannot wrap (2^-126 is far below any
+// value that survives quantization).
+__device__ __forceinline__ f2 ex2_poly2(f2 x) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer in the low bits
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
+  const f2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const f2 jf = fadd2(t, make_float2(-kMagic, -kMagic));  // rint(x), exact
+  const f2 f = fadd2(x, make_float2(-jf.x, -jf.y));       // x - rint(x), exact (Sterbenz)
+  f2 p = make_float2(0.001327647129073739f, 0.001327647129073739f);
+  p = ffma2(p, f, make_float2(0.009675541892647743f, 0.009675541892647743f));
+  p = ffma2(p, f, make_float2(0.05550713464617729f, 0.05550713464617729f));
+  p = ffma2(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
+  p = ffma2(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
+  p = ffma2(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 template <uint32_t N>
@@ -200,7 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x >= 128 && threadIdx.x < 256) {  // exact reciprocal of every E4M3 scale; 0 for s = 0
     const int c = threadIdx.x - 128;
     const float s = e4m3_to_f32((uint32_t)c);
-    reinterpret_cast<float*>(smem + L::oLut)[c] = (s == 0.0f || c == 0x7F) ? 0.0f : __frcp_rn(s);
+    // -log2(s) per E4M3 scale code (y = P̃2/s = 2^(x - log2 s)); an s = 0 block uses 2^10 and its
+    // codes are forced to 0 (reading c5), its row-sum contribution is Σy·2^-10.
+    float* lut = reinterpret_cast<float*>(smem + L::oLut);
+    const bool zero = (s == 0.0f || c == 0x7F);
+    lut[c] = zero ? 10.0f : -log2f(s);
+    lut[128 + c] = zero ? 0x1p-10f : s;
   }
   tc_fence_before();
   __syncthreads();
@@ -322,7 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kv0 = j * 128;
       const bool masked = kv0 + 128 > a.N || (a.causal && j == qt);
       const int lim = a.causal ? min(a.N - 1, q_row) - kv0 : a.N - 1 - kv0;  // last visible key in tile
-      // ---- pass 1: 16-key block maxima of S (reused for the row max and for s_P2)
+      // ---- pass 1: 16-key block maxima of S (reused for the row max and for s_P2).  Masked keys are set
+      //      to -inf and written back to TMEM so pass 2 needs no masking code.
       float bmax[8];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -331,8 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* f = reinterpret_cast<float*>(v);
         if (masked) {
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (32 * c + t > lim) f[t] = -INFINITY;
+          for (int t = 0; t < 32; ++t) f[t] = (32 * c + t > lim) ? -INFINITY : f[t];
+          tmem_st_32x32b_x32(s_addr + 32 * c, v);
         }
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
@@ -340,57 +371,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
       const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb)
-      const f2 nbx2 = make_float2(nb, nb);
-      mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
-      // ---- pass 2: P̃2, rowsum(P̃2), φ(P̃2) per 16-key block, P̂2 / s_P2 to smem
-      f2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-      uint32_t scw[2] = {0u, 0u};
+      // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
+      //      s = E4M3(amax/6); pass 2 then produces y = P̃2/s directly as 2^(S·sl2 + nb - log2 s).
+      float nbb[8], sdec[8];
+      uint32_t scw[2] = {0u, 0u}, zmask = 0u;
 #pragma unroll
+      for (int blk = 0; blk < 8; ++blk) {
+        const float amax = ex2(fmaf(bmax[blk], sl2, nb));
+        const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
+        nbb[blk] = nb + lds_f32(lut_s + 4 * sc);
+        sdec[blk] = lds_f32(lut_s + 512 + 4 * sc);
+        scw[blk >> 2] |= sc << (8 * (blk & 3));
+        zmask |= (sc == 0u ? 1u : 0u) << blk;
+      }
+      if (masked) tmem_st_wait();
+      mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
+      // ---- pass 2: y = P̃2/s, codes E2M1(y), rowsum(P̃2) = Σ_blk s_blk·Σy; one 32-key chunk per iteration,
+      //      kPolyPairsPer4 of every 4 exp2 pairs on the FMA pipe, the rest on MUFU
+      float rowsum = 0.0f;
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
+        const float nA = c == 0 ? nbb[0] : c == 1 ? nbb[2] : c == 2 ? nbb[4] : nbb[6];
+        const float nB = c == 0 ? nbb[1] : c == 1 ? nbb[3] : c == 2 ? nbb[5] : nbb[7];
+        const float sA = c == 0 ? sdec[0] : c == 1 ? sdec[2] : c == 2 ? sdec[4] : sdec[6];
+        const float sB = c == 0 ? sdec[1] : c == 1 ? sdec[3] : c == 2 ? sdec[5] : sdec[7];
         uint32_t v[32];
         tmem_ld32(s_addr + 32 * c, v);
-        float* f = reinterpret_cast<float*>(v);
-        if (masked) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (32 * c + t > lim) f[t] = -INFINITY;
-        }
-        float p[32];
-#pragma unroll
-        for (int t = 0; t < 32; t += 2) {
-          const f2 x = ffma2(make_float2(f[t], f[t + 1]), sl2x2, nbx2);
-          p[t] = ex2(x.x);
-          p[t + 1] = ex2(x.y);
-        }
-#pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-          acc0 = fadd2(acc0, make_float2(p[t], p[t + 1]));
-          acc1 = fadd2(acc1, make_float2(p[t + 2], p[t + 3]));
-        }
         uint32_t w[4];
 #pragma unroll
         for (int hb = 0; hb < 2; ++hb) {
-          const int blk = 2 * c + hb;
-          const float amax = ex2(fmaf(bmax[blk], sl2, nb));  // == max of the block's P̃2 values
-          const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
-          const float rcp = lds_f32(lut_s + 4 * sc);
-          const f2 rr = make_float2(rcp, rcp);
+          const float nbh = hb ? nB : nA;
+          const f2 nbx2 = make_float2(nbh, nbh);
           f2 y[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) y[i] = fmul2(make_float2(p[16 * hb + 2 * i], p[16 * hb + 2 * i + 1]), rr);
-          w[2 * hb] = cvt_e2m1x8(y[0].x, y[0].y, y[1].x, y[1].y, y[2].x, y[2].y, y[3].x, y[3].y);
-          w[2 * hb + 1] = cvt_e2m1x8(y[4].x, y[4].y, y[5].x, y[5].y, y[6].x, y[6].y, y[7].x, y[7].y);
-          scw[blk >> 2] |= sc << (8 * (blk & 3));
+          for (int i = 0; i < 8; ++i) {
+            const f2 x = ffma2(make_float2(__uint_as_float(v[16 * hb + 2 * i]), __uint_as_float(v[16 * hb + 2 * i + 1])),
+                               sl2x2, nbx2);
+            y[i] = ((i & 3) < kPolyPairsPer4) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          }
+          const f2 s01 = fadd2(fadd2(y[0], y[1]), fadd2(y[2], y[3]));
+          const f2 s23 = fadd2(fadd2(y[4], y[5]), fadd2(y[6], y[7]));
+          const f2 sy = fadd2(s01, s23);
+          rowsum = fmaf(hb ? sB : sA, sy.x + sy.y, rowsum);
+          const bool zb = (zmask >> (2 * c + hb)) & 1u;
+          const uint32_t w0 = cvt_e2m1x8(y[0].x, y[0].y, y[1].x, y[1].y, y[2].x, y[2].y, y[3].x, y[3].y);
+          const uint32_t w1 = cvt_e2m1x8(y[4].x, y[4].y, y[5].x, y[5].y, y[6].x, y[6].y, y[7].x, y[7].y);
+          w[2 * hb] = zb ? 0u : w0;
+          w[2 * hb + 1] = zb ? 0u : w1;
         }
         // 16-byte chunk c = keys [32c, 32c+32) of row r, SWIZZLE_64B (chunk ^= (row>>1)&3)
         sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
       }
       sts_u32(sPSF, scw[0]);
       sts_u32(sPSF + 512, scw[1]);
-      const f2 acc = fadd2(acc0, acc1);
       const int slot = j % kXSlots;
       sts_f32(xchg_s + slot * 1024, tmax);
-      sts_f32(xchg_s + slot * 1024 + 512, acc.x + acc.y);
+      sts_f32(xchg_s + slot * 1024 + 512, rowsum);
       tc_fence_before();
       fence_proxy_async_smem();
       mbar_arrive(&p_full[pb]);
