@@ -112,7 +112,7 @@ def load_traffic(workload: str):
     return None
 
 
-def cpu_baseline(args, d, timeout_s=20.0):
+def cpu_baseline(args, d, timeout_s=12.0):
     """The oracle as it stands (oracle/, plain C fp64 + OpenMP) on a bounded sample of the workload:
     quantize head 0, then Algorithm 1 for R query rows of it.  TOPS-equivalent = 4·R·N·d / t."""
     import numpy as np
@@ -126,16 +126,17 @@ def cpu_baseline(args, d, timeout_s=20.0):
     t0 = time.perf_counter()
     h = oracle.quantize_head(Q, K, V)
     tq = time.perf_counter() - t0
-    # calibrate on a few rows, then size the sample to ~timeout_s/2 of work
-    rows = np.linspace(0, N - 1, max(nthr, 4)).astype(np.int32)
-    t0 = time.perf_counter()
-    oracle.attn_fwd([h], causal=args.causal, scale=1 / math.sqrt(d), rows=rows)
-    t1 = time.perf_counter() - t0
-    R = int(min(max(len(rows), len(rows) * (timeout_s / 2) / max(t1, 1e-3)), N))
-    rows = np.linspace(0, N - 1, R).astype(np.int32)
-    t0 = time.perf_counter()
-    oracle.attn_fwd([h], causal=args.causal, scale=1 / math.sqrt(d), rows=rows)
-    ta = time.perf_counter() - t0
+    # grow the row sample until one timed call takes about timeout_s (or covers all rows)
+    R = max(4 * nthr, 16)
+    while True:
+        rows = np.linspace(0, N - 1, min(R, N)).astype(np.int32)
+        t0 = time.perf_counter()
+        oracle.attn_fwd([h], causal=args.causal, scale=1 / math.sqrt(d), rows=rows)
+        ta = time.perf_counter() - t0
+        if ta >= 0.5 * timeout_s or R >= N:
+            break
+        R = int(R * min(8.0, timeout_s / max(ta, 1e-3)))
+    R = len(rows)
     frac = float(rows.astype(np.float64).mean() + 1) / N if args.causal else 1.0
     ops = 4.0 * R * N * d * frac
     return {"value": ops / ta / 1e12, "unit": "TOPS", "cores": nthr, "kind": "oracle",
