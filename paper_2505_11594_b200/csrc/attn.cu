@@ -164,6 +164,30 @@ __device__ __forceinline__ float max16(const float* v) {
   return fmax3(fmax3(a, b, c), fmax3(d, e, v[15]), -INFINITY);
 }
 
+#ifdef SAGE3_TRACE
+// Debug-only timeline: clock64 stamps per role r (1,2 softmax WGs, 4 correction, 5 S-MMA, 6 PV-MMA), KV tile
+// j < 128 and event k < 8, recorded by one thread per role in the CTAs with blockIdx.y == 0, blockIdx.x < 2.
+__device__ unsigned long long g_trace[2][8][128][8];
+#define SAGE3_TRACE_EV(role, j, k)                                                              \
+  do {                                                                                         \
+    if (blockIdx.y == 0 && blockIdx.x < 2 && ((threadIdx.x & 127) == 0 || threadIdx.x == 32 || threadIdx.x == 64) && (j) < 128) \
+      g_trace[blockIdx.x][role][j][k] = clock64();                                             \
+  } while (0)
+// per-warp variant: lane 0 of each warp of the role's warpgroup records event k0 + (warp & 3)
+#define SAGE3_TRACE_WARP(role, j, k0)                                                           \
+  do {                                                                                         \
+    if (blockIdx.y == 0 && blockIdx.x < 2 && (threadIdx.x & 31) == 0 && (j) < 128)               \
+      g_trace[blockIdx.x][role][j][(k0) + ((threadIdx.x >> 5) & 3)] = clock64();               \
+  } while (0)
+#else
+#define SAGE3_TRACE_WARP(role, j, k0) \
+  do {                                \
+  } while (0)
+#define SAGE3_TRACE_EV(role, j, k) \
+  do {                             \
+  } while (0)
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -270,20 +294,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
-    } else if (warp == 1) {
-      // ------------------------------------------------------------------ MMA issuer
+    } else if (warp == 1 || warp == 2) {
+      // ------------------------------------------------------------------ MMA issuers: warp 1 issues the S
+      // MMAs, warp 2 the PV MMAs (separate sub-partitions; disjoint scale-factor TMEM columns; each commits
+      // its own completions)
       if (elect_one()) {
         constexpr uint32_t kQKLayout = D == 128 ? kLayoutSw64 : kLayoutSw32;
         constexpr uint32_t idesc_s = make_idesc_nvf4(128, 128);
         constexpr uint32_t idesc_pv = make_idesc_nvf4(128, D);
-        mbar_wait(q_full, 0);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < D / 64; ++ks) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * ks, sf_desc(sQSF + 512 * ks));
         auto issue_s = [&](int j) {
           const int b = j % kSBufs, st = j % kKStages;
+          SAGE3_TRACE_EV(5, j, 0);
           mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
+          SAGE3_TRACE_EV(5, j, 1);
           mbar_wait(&k_full[st], (uint32_t)(j / kKStages) & 1u);
+          SAGE3_TRACE_EV(5, j, 2);
           tc_fence_after();
           const uint8_t* sK = smem + L::oK + st * L::kKSlot;
           const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
@@ -297,11 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           mma_commit(&k_empty[st]);
           mma_commit(&s_full[b]);
+          SAGE3_TRACE_EV(5, j, 3);
         };
         auto issue_pv = [&](int j) {
           const int b = j % kSBufs, pb = j % kPBufs, st = j % kVStages;
+          SAGE3_TRACE_EV(6, j, 0);
           mbar_wait(&p_full[pb], (uint32_t)(j / kPBufs) & 1u);
+          SAGE3_TRACE_EV(6, j, 1);
           mbar_wait(&v_full[st], (uint32_t)(j / kVStages) & 1u);
+          SAGE3_TRACE_EV(6, j, 2);
           tc_fence_after();
           const uint8_t* sP = smem + L::oP + pb * L::kPBytes;
           const uint8_t* sV = smem + L::oV + st * L::kVBytes;
@@ -321,20 +350,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&v_empty[st]);
           mma_commit(&p_empty[pb]);
           mma_commit(&pv_full[b]);
+          SAGE3_TRACE_EV(6, j, 3);
         };
-        issue_s(0);
-        if (nkv > 1) issue_s(1);
-        for (int j = 0; j < nkv; ++j) {
-          if (j + 2 < nkv) issue_s(j + 2);  // buffer (j+2)%3 held PV_{j-1}; freed by the correction
-          issue_pv(j);
+        if (warp == 1) {
+          mbar_wait(q_full, 0);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < D / 64; ++ks) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * ks, sf_desc(sQSF + 512 * ks));
+          for (int j = 0; j < nkv; ++j) issue_s(j);  // S_j into buffer j%3 once the correction freed it
+        } else {
+          for (int j = 0; j < nkv; ++j) issue_pv(j);
         }
       }
       __syncwarp();
     }
-  } else if (wg <= 2) {
+  } else if (wg >= 2) {
     // -------------------------------------------------------------------- softmax + two-level P quant
     setmaxnreg_inc<136>();
-    const int par = wg - 1;                 // this warpgroup's KV-tile parity
+    const int par = wg - 2;                 // this warpgroup's KV-tile parity
     const int r = threadIdx.x - 128 * wg;   // query row in the tile == TMEM lane
     const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
@@ -347,18 +380,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t s_addr = lane_base + 128 * sb;
       const uint32_t sP = smem_u32(smem + L::oP + pb * L::kPBytes) + r * 64;
       const uint32_t sPSF = smem_u32(smem + L::oPSF + pb * L::kPSF) + (r & 31) * 16 + (r >> 5) * 4;
+      SAGE3_TRACE_EV(1 + par, j, 0);
       mbar_wait(&s_full[sb], (uint32_t)(j / kSBufs) & 1u);
+      SAGE3_TRACE_EV(1 + par, j, 1);
       tc_fence_after();
       const int kv0 = j * 128;
       const bool masked = kv0 + 128 > a.N || (a.causal && j == qt);
       const int lim = a.causal ? min(a.N - 1, q_row) - kv0 : a.N - 1 - kv0;  // last visible key in tile
       // ---- pass 1: 16-key block maxima of S (reused for the row max and for s_P2).  Masked keys are set
-      //      to -inf and written back to TMEM so pass 2 needs no masking code.
+      //      to -inf and written back to TMEM so pass 2 needs no masking code.  Two 32-column TMEM loads
+      //      are in flight at a time.
       float bmax[8];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(s_addr + 32 * c, v);
+      auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
         if (masked) {
 #pragma unroll
@@ -367,10 +400,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
+      };
+      {
+        uint32_t va[32], vb[32];
+#pragma unroll
+        for (int c = 0; c < 4; c += 2) {
+          tmem_ld_32x32b_x32(s_addr + 32 * c, va);
+          tmem_ld_32x32b_x32(s_addr + 32 * c + 32, vb);
+          tmem_ld_wait_regs(va);
+          tmem_ld_wait_regs(vb);
+          pass1(c, va);
+          pass1(c + 1, vb);
+        }
       }
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
       const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb)
+      if (masked) tmem_st_wait();
+      uint32_t va[32], vb[32];
+      tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
       // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
       //      s = E4M3(amax/6); pass 2 then produces y = P̃2/s directly as 2^(S·sl2 + nb - log2 s).
       float nbb[8], sdec[8];
@@ -384,43 +432,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         scw[blk >> 2] |= sc << (8 * (blk & 3));
         zmask |= (sc == 0u ? 1u : 0u) << blk;
       }
-      if (masked) tmem_st_wait();
+      SAGE3_TRACE_EV(1 + par, j, 2);
       mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
-      // ---- pass 2: y = P̃2/s, codes E2M1(y), rowsum(P̃2) = Σ_blk s_blk·Σy; one 32-key chunk per iteration,
-      //      kPolyPairsPer4 of every 4 exp2 pairs on the FMA pipe, the rest on MUFU
+      SAGE3_TRACE_EV(1 + par, j, 3);
+      // ---- pass 2: y = P̃2/s, codes E2M1(y), rowsum(P̃2) = Σ_blk s_blk·Σy.  Software-pipelined over the four
+      //      32-key chunks: the exp2 of chunk c (MUFU / FMA-pipe polynomial) sits in the same straight-line
+      //      block as the sums, E2M1 converts and smem store of chunk c-1, so the scheduler can interleave
+      //      MUFU with independent FMA/ALU work.
       float rowsum = 0.0f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      auto exps = [&](int c, const uint32_t(&v)[32], f2(&y)[16]) {
         const float nA = c == 0 ? nbb[0] : c == 1 ? nbb[2] : c == 2 ? nbb[4] : nbb[6];
         const float nB = c == 0 ? nbb[1] : c == 1 ? nbb[3] : c == 2 ? nbb[5] : nbb[7];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float nbh = i < 8 ? nA : nB;
+          const f2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2,
+                             make_float2(nbh, nbh));
+          y[i] = ((i & 3) < kPolyPairsPer4) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+        }
+      };
+      auto finish = [&](int c, const f2(&y)[16]) {
         const float sA = c == 0 ? sdec[0] : c == 1 ? sdec[2] : c == 2 ? sdec[4] : sdec[6];
         const float sB = c == 0 ? sdec[1] : c == 1 ? sdec[3] : c == 2 ? sdec[5] : sdec[7];
-        uint32_t v[32];
-        tmem_ld32(s_addr + 32 * c, v);
         uint32_t w[4];
 #pragma unroll
         for (int hb = 0; hb < 2; ++hb) {
-          const float nbh = hb ? nB : nA;
-          const f2 nbx2 = make_float2(nbh, nbh);
-          f2 y[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const f2 x = ffma2(make_float2(__uint_as_float(v[16 * hb + 2 * i]), __uint_as_float(v[16 * hb + 2 * i + 1])),
-                               sl2x2, nbx2);
-            y[i] = ((i & 3) < kPolyPairsPer4) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          }
-          const f2 s01 = fadd2(fadd2(y[0], y[1]), fadd2(y[2], y[3]));
-          const f2 s23 = fadd2(fadd2(y[4], y[5]), fadd2(y[6], y[7]));
+          const f2* yy = y + 8 * hb;
+          const f2 s01 = fadd2(fadd2(yy[0], yy[1]), fadd2(yy[2], yy[3]));
+          const f2 s23 = fadd2(fadd2(yy[4], yy[5]), fadd2(yy[6], yy[7]));
           const f2 sy = fadd2(s01, s23);
           rowsum = fmaf(hb ? sB : sA, sy.x + sy.y, rowsum);
           const bool zb = (zmask >> (2 * c + hb)) & 1u;
-          const uint32_t w0 = cvt_e2m1x8(y[0].x, y[0].y, y[1].x, y[1].y, y[2].x, y[2].y, y[3].x, y[3].y);
-          const uint32_t w1 = cvt_e2m1x8(y[4].x, y[4].y, y[5].x, y[5].y, y[6].x, y[6].y, y[7].x, y[7].y);
+          const uint32_t w0 = cvt_e2m1x8(yy[0].x, yy[0].y, yy[1].x, yy[1].y, yy[2].x, yy[2].y, yy[3].x, yy[3].y);
+          const uint32_t w1 = cvt_e2m1x8(yy[4].x, yy[4].y, yy[5].x, yy[5].y, yy[6].x, yy[6].y, yy[7].x, yy[7].y);
           w[2 * hb] = zb ? 0u : w0;
           w[2 * hb + 1] = zb ? 0u : w1;
         }
         // 16-byte chunk c = keys [32c, 32c+32) of row r, SWIZZLE_64B (chunk ^= (row>>1)&3)
         sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
+      };
+      {
+        f2 ya[16], yb[16];
+        tmem_ld_wait_regs(va);
+        tmem_ld_32x32b_x32(s_addr + 32, vb);
+        exps(0, va, ya);
+        tmem_ld_wait_regs(vb);
+        tmem_ld_32x32b_x32(s_addr + 64, va);
+        exps(1, vb, yb);
+        finish(0, ya);
+        tmem_ld_wait_regs(va);
+        tmem_ld_32x32b_x32(s_addr + 96, vb);
+        exps(2, va, ya);
+        finish(1, yb);
+        tmem_ld_wait_regs(vb);
+        exps(3, vb, yb);
+        finish(2, ya);
+        finish(3, yb);
       }
       sts_u32(sPSF, scw[0]);
       sts_u32(sPSF + 512, scw[1]);
@@ -430,6 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       fence_proxy_async_smem();
       mbar_arrive(&p_full[pb]);
+      SAGE3_TRACE_WARP(1 + par, j, 4);
       mbar_arrive(&x_full[slot]);
     }
   } else {
@@ -439,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     //   w_j = 2^{sl2 (tmax_j − mref)} / 2688  (= s_P1 · Π α relative to mref)
     // which is Alg1 L9-L11 up to fp32 rounding: O/l and lse are independent of the reference.
     setmaxnreg_inc<200>();
-    const int r = threadIdx.x - 384;
+    const int r = threadIdx.x - 128;
     const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
@@ -450,7 +518,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = 0; c < D / 2; ++c) o[c] = make_float2(0.f, 0.f);
     for (int j = 0; j < nkv; ++j) {
       const int slot = j % kXSlots, b = j % kSBufs;
+      SAGE3_TRACE_EV(4, j, 0);
       mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
+      SAGE3_TRACE_EV(4, j, 1);
       const float tmax = lds_f32(xchg_s + slot * 1024);
       const float rs2 = lds_f32(xchg_s + slot * 1024 + 512);
       const bool need = (tmax - mref) * sl2 > 8.0f;  // true on the first tile (mref = -inf)
@@ -467,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
       mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
+      SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < D / 16; ++c) {
@@ -478,6 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&b_empty[b]);
+      SAGE3_TRACE_EV(4, j, 3);
     }
     const float m = mref;
     // Alg1 L13: O_i = diag(l)^-1 O_i
@@ -581,5 +653,12 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream) {
   return a.d == 128 ? launch_d<128>(a, stream) : launch_d<64>(a, stream);
 }
+
+#ifdef SAGE3_TRACE
+extern "C" int sage3_debug_trace_copy(void* host, size_t bytes) {
+  if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);
+  return (int)cudaMemcpyFromSymbol(host, g_trace, bytes);
+}
+#endif
 
 }  // namespace sage3
