@@ -39,6 +39,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     target = out or LIB
     if out is None and not force and not stale():
         return LIB
+    os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
     tmp = target + f".tmp{os.getpid()}"
     cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
            "-I", os.path.join(ROOT, "include"), "-I", CSRC,

@@ -44,10 +44,14 @@ using namespace ptx;
 constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
-#ifndef SAGE3_POLY_PAIRS_PER4
-#define SAGE3_POLY_PAIRS_PER4 1
+#ifndef SAGE3_POLY_MASK
+#define SAGE3_POLY_MASK 0x1111
 #endif
-constexpr int kPolyPairsPer4 = SAGE3_POLY_PAIRS_PER4;  // of every 4 exp2 pairs in pass 2, this many use the polynomial
+#ifndef SAGE3_POLY_DEGREE
+#define SAGE3_POLY_DEGREE 4
+#endif
+// bit i set: exp2 pair i of each 32-key chunk (16 pairs) runs on the FMA pipe (polynomial), else on MUFU
+constexpr uint32_t kPolyMask = SAGE3_POLY_MASK;
 constexpr int kThreads = 512;
 constexpr float kOneSixth = 0x1.555556p-3f;  // fl32(1/6)
 constexpr float kLog2e = 1.4426950408889634f;
@@ -79,8 +83,7 @@ struct Layout {
   static constexpr int oVSF = oKSF + kKStages * kQKSF;
   static constexpr int oPSF = oVSF + kVStages * kVSF;
   static constexpr int oXchg = oPSF + kPBufs * kPSF;            // float [kXSlots][2][128]: tmax_j, rowsum(P̃2_j)
-  static constexpr int oLut = oXchg + kXSlots * 2 * 128 * 4;  // float [2][128]: -log2(s), s per E4M3 code
-  static constexpr int oBar = oLut + 2 * 128 * 4;
+  static constexpr int oBar = oXchg + kXSlots * 2 * 128 * 4;
   static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + kXSlots;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
@@ -104,12 +107,21 @@ __device__ __forceinline__ f2 ex2_poly2(f2 x) {
   const f2 t = fadd2(x, make_float2(kMagic, kMagic));
   const f2 jf = fadd2(t, make_float2(-kMagic, -kMagic));  // rint(x), exact
   const f2 f = fadd2(x, make_float2(-jf.x, -jf.y));       // x - rint(x), exact (Sterbenz)
+#if SAGE3_POLY_DEGREE == 4
+  // degree 4 (max rel. error 2.7e-6: below the E2M1 decision noise, reading c14)
+  f2 p = make_float2(0.009570094756782055f, 0.009570094756782055f);
+  p = ffma2(p, f, make_float2(0.05591786280274391f, 0.05591786280274391f));
+  p = ffma2(p, f, make_float2(0.240247443318367f, 0.240247443318367f));
+  p = ffma2(p, f, make_float2(0.6931217908859253f, 0.6931217908859253f));
+  p = ffma2(p, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
+#else
   f2 p = make_float2(0.001327647129073739f, 0.001327647129073739f);
   p = ffma2(p, f, make_float2(0.009675541892647743f, 0.009675541892647743f));
   p = ffma2(p, f, make_float2(0.05550713464617729f, 0.05550713464617729f));
   p = ffma2(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
   p = ffma2(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
   p = ffma2(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+#endif
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
@@ -145,11 +157,6 @@ __device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[16]) {
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   tmem_ld_32x32b_x16(taddr, v);
-  tmem_ld_wait_regs(v);
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  tmem_ld_32x32b_x32(taddr, v);
   tmem_ld_wait_regs(v);
 }
 
@@ -194,6 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tm_v, const AttnArgs a) {
   using L = Layout<D>;
   extern __shared__ uint8_t smem_raw[];
+  // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
+  __shared__ __align__(1024) float2 s_lut[128];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   uint8_t* sQ = smem + L::oQ;
@@ -231,13 +240,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < kSBufs; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&pv_full[b], 1);
-      mbar_init(&b_empty[b], 128);
+      mbar_init(&b_empty[b], 4);  // one arrival per correction warp
     }
     for (int b = 0; b < kPBufs; ++b) {
-      mbar_init(&p_full[b], 128);
+      mbar_init(&p_full[b], 4);  // one arrival per softmax warp
       mbar_init(&p_empty[b], 1);
     }
-    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 128);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 4);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -249,12 +258,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x >= 128 && threadIdx.x < 256) {  // exact reciprocal of every E4M3 scale; 0 for s = 0
     const int c = threadIdx.x - 128;
     const float s = e4m3_to_f32((uint32_t)c);
-    // -log2(s) per E4M3 scale code (y = P̃2/s = 2^(x - log2 s)); an s = 0 block uses 2^10 and its
-    // codes are forced to 0 (reading c5), its row-sum contribution is Σy·2^-10.
-    float* lut = reinterpret_cast<float*>(smem + L::oLut);
+    // -log2(s) per E4M3 scale code (y = P̃2/s = 2^(x - log2 s)); an s = 0 block uses 2^10 (its codes are
+    // multiplied by s = 0 in the MMA, reading c5), its row-sum contribution is Σy·2^-10.
     const bool zero = (s == 0.0f || c == 0x7F);
-    lut[c] = zero ? 10.0f : -log2f(s);
-    lut[128 + c] = zero ? 0x1p-10f : s;
+    s_lut[c] = make_float2(zero ? 10.0f : -log2f(s), zero ? 0x1p-10f : s);
   }
   tc_fence_before();
   __syncthreads();
@@ -371,7 +378,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = threadIdx.x - 128 * wg;   // query row in the tile == TMEM lane
     const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-    const uint32_t lut_s = smem_u32(smem + L::oLut);
     const float sl2 = a.scale * kLog2e;
     const f2 sl2x2 = make_float2(sl2, sl2);
     const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
@@ -409,8 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x32(s_addr + 32 * c + 32, vb);
           tmem_ld_wait_regs(va);
           tmem_ld_wait_regs(vb);
+          SAGE3_TRACE_EV(par ? 3 : 0, j, c);
           pass1(c, va);
           pass1(c + 1, vb);
+          SAGE3_TRACE_EV(par ? 3 : 0, j, c + 1);
         }
       }
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
@@ -420,18 +428,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t va[32], vb[32];
       tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
       // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
-      //      s = E4M3(amax/6); pass 2 then produces y = P̃2/s directly as 2^(S·sl2 + nb - log2 s).
+      //      s = E4M3(amax/6), two blocks per convert; pass 2 then produces y = P̃2/s directly as
+      //      2^(S·sl2 + nb - log2 s) with (-log2 s, s) from a 128-entry table indexed by the E4M3 code.
+      //      A block whose scale underflows to 0 (reading c5) keeps whatever codes pass 2 produces: the
+      //      PV MMA multiplies them by s = 0, so they contribute exactly 0, as the oracle's zero codes do;
+      //      its table entry (10, 2^-10) keeps its unquantized P̃2 in the row sum (reading c9).
       float nbb[8], sdec[8];
-      uint32_t scw[2] = {0u, 0u}, zmask = 0u;
+      uint32_t scw[2];
+      {
+        uint32_t c2[4];
 #pragma unroll
-      for (int blk = 0; blk < 8; ++blk) {
-        const float amax = ex2(fmaf(bmax[blk], sl2, nb));
-        const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
-        nbb[blk] = nb + lds_f32(lut_s + 4 * sc);
-        sdec[blk] = lds_f32(lut_s + 512 + 4 * sc);
-        scw[blk >> 2] |= sc << (8 * (blk & 3));
-        zmask |= (sc == 0u ? 1u : 0u) << blk;
+        for (int k = 0; k < 4; ++k) {
+          const f2 e = ffma2(make_float2(bmax[2 * k], bmax[2 * k + 1]), sl2x2, make_float2(nb, nb));
+          const f2 q = fmul2(make_float2(ex2(e.x), ex2(e.y)), make_float2(kOneSixth, kOneSixth));
+          c2[k] = cvt_e4m3x2(q.x, q.y);  // block 2k in the low byte
+        }
+        scw[0] = __byte_perm(c2[0], c2[1], 0x5410);
+        scw[1] = __byte_perm(c2[2], c2[3], 0x5410);
+#pragma unroll
+        for (int blk = 0; blk < 8; ++blk) {
+          const float2 t = s_lut[(scw[blk >> 2] >> (8 * (blk & 3))) & 0xFFu];
+          nbb[blk] = nb + t.x;
+          sdec[blk] = t.y;
+        }
       }
+      SAGE3_TRACE_EV(par ? 3 : 0, j, 4);
       SAGE3_TRACE_EV(1 + par, j, 2);
       mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
       SAGE3_TRACE_EV(1 + par, j, 3);
@@ -448,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float nbh = i < 8 ? nA : nB;
           const f2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2,
                              make_float2(nbh, nbh));
-          y[i] = ((i & 3) < kPolyPairsPer4) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          y[i] = ((kPolyMask >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
         }
       };
       auto finish = [&](int c, const f2(&y)[16]) {
@@ -462,11 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const f2 s23 = fadd2(fadd2(yy[4], yy[5]), fadd2(yy[6], yy[7]));
           const f2 sy = fadd2(s01, s23);
           rowsum = fmaf(hb ? sB : sA, sy.x + sy.y, rowsum);
-          const bool zb = (zmask >> (2 * c + hb)) & 1u;
-          const uint32_t w0 = cvt_e2m1x8(yy[0].x, yy[0].y, yy[1].x, yy[1].y, yy[2].x, yy[2].y, yy[3].x, yy[3].y);
-          const uint32_t w1 = cvt_e2m1x8(yy[4].x, yy[4].y, yy[5].x, yy[5].y, yy[6].x, yy[6].y, yy[7].x, yy[7].y);
-          w[2 * hb] = zb ? 0u : w0;
-          w[2 * hb + 1] = zb ? 0u : w1;
+          w[2 * hb] = cvt_e2m1x8(yy[0].x, yy[0].y, yy[1].x, yy[1].y, yy[2].x, yy[2].y, yy[3].x, yy[3].y);
+          w[2 * hb + 1] = cvt_e2m1x8(yy[4].x, yy[4].y, yy[5].x, yy[5].y, yy[6].x, yy[6].y, yy[7].x, yy[7].y);
         }
         // 16-byte chunk c = keys [32c, 32c+32) of row r, SWIZZLE_64B (chunk ^= (row>>1)&3)
         sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
@@ -474,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         f2 ya[16], yb[16];
         tmem_ld_wait_regs(va);
+        SAGE3_TRACE_EV(par ? 3 : 0, j, 5);
         tmem_ld_32x32b_x32(s_addr + 32, vb);
         exps(0, va, ya);
         tmem_ld_wait_regs(vb);
@@ -485,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         exps(2, va, ya);
         finish(1, yb);
         tmem_ld_wait_regs(vb);
+        SAGE3_TRACE_EV(par ? 3 : 0, j, 6);
         exps(3, vb, yb);
         finish(2, ya);
         finish(3, yb);
@@ -496,9 +516,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       sts_f32(xchg_s + slot * 1024 + 512, rowsum);
       tc_fence_before();
       fence_proxy_async_smem();
-      mbar_arrive(&p_full[pb]);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&p_full[pb]);
+        mbar_arrive(&x_full[slot]);
+      }
       SAGE3_TRACE_WARP(1 + par, j, 4);
-      mbar_arrive(&x_full[slot]);
     }
   } else {
     // -------------------------------------------------------------------- correction + epilogue
@@ -548,7 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           o[8 * c + i] = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), ww, o[8 * c + i]);
       }
       tc_fence_before();
-      mbar_arrive(&b_empty[b]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&b_empty[b]);
       SAGE3_TRACE_EV(4, j, 3);
     }
     const float m = mref;

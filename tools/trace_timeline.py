@@ -72,3 +72,10 @@ for j in range(8, 20):
     sm = 1 + j % 2
     w0 = t[sm, j, 1]
     print(f" tile {j:2d} WG{sm-1}: " + " ".join(f"{int(t[sm, j, 4 + w] - w0):6d}" for w in range(4)))
+
+print("\nsoftmax sub-events (relative to the warpgroup's S wake k1): ld01-wait, pass1a, ld23-wait, pass1b(tmax), scales, pass2-ld0-wait, pass2-ld3-wait, P ready")
+for j in range(8, 20):
+    sm = 1 + j % 2
+    sub = 0 if sm == 1 else 3
+    w0 = t[sm, j, 1]
+    print(f" tile {j:2d} WG{sm-1}: " + " ".join(f"{int(t[sub, j, k] - w0):6d}" for k in range(7)) + f" {int(t[sm, j, 4] - w0):6d}")
