@@ -32,6 +32,7 @@
 #include <cmath>
 #include <cstdint>
 #include <mutex>
+#include <type_traits>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -53,6 +54,15 @@ constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j
 // bit i set: exp2 pair i of each 32-key chunk (16 pairs) runs on the FMA pipe (polynomial), else on MUFU
 constexpr uint32_t kPolyMask = SAGE3_POLY_MASK;
 constexpr int kThreads = 512;
+// Per-thread register budgets after setmaxnreg (one warp of each warpgroup per SM sub-partition:
+// kRegWG0 + 2 kRegSoftmax + kRegCorrection = 512 = 64K registers / 128 lanes).
+#ifndef SAGE3_REG_WG0
+#define SAGE3_REG_WG0 40
+#define SAGE3_REG_SOFTMAX 136
+#define SAGE3_REG_CORRECTION 200
+#endif
+constexpr uint32_t kRegWG0 = SAGE3_REG_WG0, kRegSoftmax = SAGE3_REG_SOFTMAX, kRegCorrection = SAGE3_REG_CORRECTION;
+static_assert(kRegWG0 + 2 * kRegSoftmax + kRegCorrection <= 512, "register budget");
 constexpr float kOneSixth = 0x1.555556p-3f;  // fl32(1/6)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_2688 = 11.392317422778761f;  // log2(448 * 6)
@@ -270,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int wg = warp >> 2;
 
   if (wg == 0) {
-    setmaxnreg_dec<40>();
+    setmaxnreg_dec<kRegWG0>();
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer: Q, K
       if (elect_one()) {
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (wg >= 2) {
     // -------------------------------------------------------------------- softmax + two-level P quant
-    setmaxnreg_inc<136>();
+    setmaxnreg_inc<kRegSoftmax>();
     const int par = wg - 2;                 // this warpgroup's KV-tile parity
     const int r = threadIdx.x - 128 * wg;   // query row in the tile == TMEM lane
     const int q_row = qt * 128 + r;
@@ -381,7 +391,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = a.scale * kLog2e;
     const f2 sl2x2 = make_float2(sl2, sl2);
     const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
-    for (int j = par; j < nkv; j += 2) {
+    // One KV tile (Alg1 L8-L10 for this warpgroup's rows).  Only the last tile can need masking (keys >= N,
+    // or the causal diagonal), so it is a separate instantiation outside the hot loop: the loop body is
+    // straight-line code with no masking branches (instruction-cache friendly).
+    auto tile = [&](const int j, auto masked_tag) {
+      constexpr bool masked = decltype(masked_tag)::value;
       const int sb = j % kSBufs, pb = j % kPBufs;
       const uint32_t s_addr = lane_base + 128 * sb;
       const uint32_t sP = smem_u32(smem + L::oP + pb * L::kPBytes) + r * 64;
@@ -391,7 +405,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       SAGE3_TRACE_EV(1 + par, j, 1);
       tc_fence_after();
       const int kv0 = j * 128;
-      const bool masked = kv0 + 128 > a.N || (a.causal && j == qt);
       const int lim = a.causal ? min(a.N - 1, q_row) - kv0 : a.N - 1 - kv0;  // last visible key in tile
       // ---- pass 1: 16-key block maxima of S (reused for the row max and for s_P2).  Masked keys are set
       //      to -inf and written back to TMEM so pass 2 needs no masking code.  Two 32-column TMEM loads
@@ -399,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float bmax[8];
       auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
-        if (masked) {
+        if constexpr (masked) {
 #pragma unroll
           for (int t = 0; t < 32; ++t) f[t] = (32 * c + t > lim) ? -INFINITY : f[t];
           tmem_st_32x32b_x32(s_addr + 32 * c, v);
@@ -424,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
       const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb)
-      if (masked) tmem_st_wait();
+      if constexpr (masked) tmem_st_wait();
       uint32_t va[32], vb[32];
       tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
       // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
@@ -522,6 +535,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&x_full[slot]);
       }
       SAGE3_TRACE_WARP(1 + par, j, 4);
+    };
+    const int last = nkv - 1;
+    const bool last_masked = last * 128 + 128 > a.N || a.causal;
+    for (int j = par; j < last; j += 2) tile(j, std::false_type{});
+    if ((last & 1) == par) {
+      if (last_masked)
+        tile(last, std::true_type{});
+      else
+        tile(last, std::false_type{});
     }
   } else {
     // -------------------------------------------------------------------- correction + epilogue
@@ -529,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // exceeds it by more than 2^8 in weight), so tile j enters with weight
     //   w_j = 2^{sl2 (tmax_j − mref)} / 2688  (= s_P1 · Π α relative to mref)
     // which is Alg1 L9-L11 up to fp32 rounding: O/l and lse are independent of the reference.
-    setmaxnreg_inc<200>();
+    setmaxnreg_inc<kRegCorrection>();
     const int r = threadIdx.x - 128;
     const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
