@@ -79,3 +79,12 @@ for j in range(8, 20):
     sub = 0 if sm == 1 else 3
     w0 = t[sm, j, 1]
     print(f" tile {j:2d} WG{sm-1}: " + " ".join(f"{int(t[sub, j, k] - w0):6d}" for k in range(7)) + f" {int(t[sm, j, 4] - w0):6d}")
+
+print("\ncorrection pass 1 (role 7): s_full wait, loads+maxes, scales+stores, p_empty wait, SF store+arrive; then O update (role 4)")
+for j in range(8, 20):
+    e = t[7, j]
+    if not e[0]:
+        continue
+    print(f" tile {j:2d}: start {int(e[0]-t0):7d}  wait_S {int(e[1]-e[0]):5d}  ld+max {int(e[2]-e[1]):5d}  scales {int(e[3]-e[2]):5d}"
+          f"  wait_Pbuf {int(e[4]-e[3]):5d}  tail {int(e[5]-e[4]):5d} | O-upd({j-2}) row-wait {int(t[4,j-2,1]-t[4,j-2,0]):5d}"
+          f" pv-wait {int(t[4,j-2,2]-t[4,j-2,1]):5d} compute {int(t[4,j-2,3]-t[4,j-2,2]):5d}")
