@@ -234,7 +234,7 @@ __device__ __forceinline__ void sts_v4(uint32_t saddr, uint32_t a, uint32_t b, u
 // Two fp32 -> packed e2m1x2 (RN, satfinite).  `lo` lands in bits [0,4), `hi` in bits [4,8).
 __device__ __forceinline__ uint32_t cvt_e2m1x2(float lo, float hi) {
   uint32_t out;
-  asm volatile(
+  asm(
       "{\n\t.reg .b8 t;\n\t"
       "cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n\t"
       "cvt.u32.u8 %0, t;\n\t}\n"
@@ -245,7 +245,7 @@ __device__ __forceinline__ uint32_t cvt_e2m1x2(float lo, float hi) {
 // Two fp32 -> packed e4m3x2 (RN, satfinite).  `lo` lands in bits [0,8).
 __device__ __forceinline__ uint32_t cvt_e4m3x2(float lo, float hi) {
   uint16_t out;
-  asm volatile("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(out) : "f"(hi), "f"(lo));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(out) : "f"(hi), "f"(lo));
   return out;
 }
 // Eight fp32 -> four packed e2m1x2 bytes in one 32-bit word (element 0 in the low nibble of byte 0).
@@ -266,7 +266,7 @@ __device__ __forceinline__ uint32_t cvt_e2m1x8(float a0, float a1, float a2, flo
 __device__ __forceinline__ float e4m3_to_f32(uint32_t code) {
   uint32_t h2;
   uint16_t c = static_cast<uint16_t>(code & 0xFF);
-  asm volatile("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(c));
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(c));
   return __half2float(__ushort_as_half(static_cast<unsigned short>(h2 & 0xFFFF)));
 }
 
