@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 
 #include "../../include/sage3.h"
 #include "internal.h"
@@ -47,6 +48,30 @@ sage3_status device_ok() {
 }
 
 int esize_of(sage3_dtype t) { return t == SAGE3_FP32 ? 4 : 2; }
+
+// sage3_forward_host pipeline: head groups and the library-owned streams (one set per device, created on
+// first use, never destroyed: they live as long as the process, like the kernels' attribute setup).
+constexpr int kHostGroups = 8;
+struct Pipe {
+  cudaStream_t s[3];
+};
+Pipe* pipe_for_current_device() {
+  static std::mutex mu;
+  static Pipe* pipes[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pipes[dev]) {
+    Pipe* p = new Pipe;
+    for (int i = 0; i < 3; ++i)
+      if (cudaStreamCreateWithFlags(&p->s[i], cudaStreamNonBlocking) != cudaSuccess) {
+        delete p;
+        return nullptr;
+      }
+    pipes[dev] = p;
+  }
+  return pipes[dev];
+}
 
 }  // namespace
 
@@ -168,25 +193,89 @@ sage3_status sage3_forward_host(const void* q_host, const void* k_host, const vo
   uint8_t *dq = take(in_b), *dk = take(in_b), *dv = take(in_b), *dout = take(o_b);
   size_t sz[7];
   sage3_fp4_qkv_sizes(B, H, N, d, sz);
-  sage3_fp4_qkv f{};
-  f.B = B, f.H = H, f.N = N, f.d = d;
-  f.q_data = take(sz[0]), f.k_data = take(sz[1]), f.v_data = take(sz[2]);
-  f.q_sf = take(sz[3]), f.k_sf = take(sz[4]), f.v_sf = take(sz[5]);
-  f.k_mean = reinterpret_cast<float*>(take(sz[6]));
-  void* ws = take(sage3_quantize_workspace_bytes(B, H, N, d));
-  cudaError_t e;
-  if ((e = cudaMemcpyAsync(dq, q_host, in_b, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
-  if ((e = cudaMemcpyAsync(dk, k_host, in_b, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
-  if ((e = cudaMemcpyAsync(dv, v_host, in_b, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
-  const int64_t sn = d, sh = (int64_t)N * d, sb = (int64_t)H * N * d;
-  sage3_tensor4 tq{dq, sb, sh, sn}, tk{dk, sb, sh, sn}, tv{dv, sb, sh, sn}, to{dout, sb, sh, sn};
-  sage3_status st = sage3_quantize_qkv(tq, tk, tv, in_dtype, B, H, N, d, &f, ws,
-                                       sage3_quantize_workspace_bytes(B, H, N, d), nullptr, stream);
+  uint8_t *q_data = take(sz[0]), *k_data = take(sz[1]), *v_data = take(sz[2]);
+  uint8_t *q_sf = take(sz[3]), *k_sf = take(sz[4]), *v_sf = take(sz[5]);
+  float* k_mean = reinterpret_cast<float*>(take(sz[6]));
+  double* ws = reinterpret_cast<double*>(take(sage3_quantize_workspace_bytes(B, H, N, d)));
+  sage3_status st = device_ok();
   if (st != SAGE3_OK) return st;
-  st = sage3_attn_fwd(&f, to, o_dtype, causal, softmax_scale, nullptr, stream);
+
+  // Pipelined over groups of heads (every (b,h) is an independent problem): the H2D copy of group g+1 and
+  // the D2H copy of group g-1 overlap the quantize + attention of group g.  Three library-owned streams
+  // per device (copy-in, compute, copy-out); per-call events order them after the caller's prior work on
+  // `stream` and make `stream` wait for the last copy-out, so the call behaves as if enqueued on `stream`.
+  Pipe* pp = pipe_for_current_device();
+  if (!pp) return cuda_fail(cudaErrorInitializationError);
+  const int BH = B * H;
+  const int G = BH < kHostGroups ? BH : kHostGroups;  // groups of consecutive flattened heads
+  const size_t head_in = (size_t)N * d * esize_of(in_dtype), head_out = (size_t)N * d * esize_of(o_dtype);
+  const size_t Np = (size_t)npad(N);
+  const int64_t sn = d, sh = (int64_t)N * d;
+  cudaError_t e = cudaSuccess;
+  cudaEvent_t start, in_done[kHostGroups], comp_done[kHostGroups], out_done;
+  int n_ev = 0;
+  auto mk = [&](cudaEvent_t* ev) {
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) ++n_ev;
+  };
+  mk(&start);
+  for (int g = 0; g < G; ++g) mk(&in_done[g]);
+  for (int g = 0; g < G; ++g) mk(&comp_done[g]);
+  mk(&out_done);
+  if (e != cudaSuccess) return cuda_fail(e);
+  cudaStream_t s_in = pp->s[0], s_cmp = pp->s[1], s_out = pp->s[2];
+  auto ck = [&](cudaError_t r) {
+    if (e == cudaSuccess && r != cudaSuccess) e = r;
+  };
+  ck(cudaEventRecord(start, s));
+  ck(cudaStreamWaitEvent(s_in, start, 0));
+  ck(cudaStreamWaitEvent(s_cmp, start, 0));
+  ck(cudaStreamWaitEvent(s_out, start, 0));
+  for (int g = 0; g < G && e == cudaSuccess && st == SAGE3_OK; ++g) {
+    const int h0 = (int)((int64_t)BH * g / G), h1 = (int)((int64_t)BH * (g + 1) / G), nh = h1 - h0;
+    // copy-in of this group's heads (q, k, v are contiguous [BH][N][d] on the host)
+    ck(cudaMemcpyAsync(dq + h0 * head_in, static_cast<const uint8_t*>(q_host) + h0 * head_in, nh * head_in,
+                       cudaMemcpyHostToDevice, s_in));
+    ck(cudaMemcpyAsync(dk + h0 * head_in, static_cast<const uint8_t*>(k_host) + h0 * head_in, nh * head_in,
+                       cudaMemcpyHostToDevice, s_in));
+    ck(cudaMemcpyAsync(dv + h0 * head_in, static_cast<const uint8_t*>(v_host) + h0 * head_in, nh * head_in,
+                       cudaMemcpyHostToDevice, s_in));
+    ck(cudaEventRecord(in_done[g], s_in));
+    ck(cudaStreamWaitEvent(s_cmp, in_done[g], 0));
+    if (e != cudaSuccess) break;
+    // quantize + attention of the group as a (1, nh) problem on slices of the full-size buffers
+    sage3_fp4_qkv f{};
+    f.B = 1, f.H = nh, f.N = N, f.d = d;
+    f.q_data = q_data + h0 * (Np * d / 2), f.k_data = k_data + h0 * (Np * d / 2), f.v_data = v_data + h0 * (Np * d / 2);
+    f.q_sf = q_sf + h0 * (Np * d / 16), f.k_sf = k_sf + h0 * (Np * d / 16), f.v_sf = v_sf + h0 * (Np * 8);
+    f.k_mean = k_mean + (size_t)h0 * d;
+    const int64_t sb = (int64_t)nh * N * d;
+    sage3_tensor4 tq{dq + h0 * head_in, sb, sh, sn}, tk{dk + h0 * head_in, sb, sh, sn};
+    sage3_tensor4 tv{dv + h0 * head_in, sb, sh, sn}, to{dout + h0 * head_out, sb, sh, sn};
+    double* wsg = ws + (size_t)h0 * (Np / 128) * d;
+    st = sage3_quantize_qkv(tq, tk, tv, in_dtype, 1, nh, N, d, &f, wsg, sage3_quantize_workspace_bytes(1, nh, N, d),
+                            nullptr, s_cmp);
+    if (st == SAGE3_OK) st = sage3_attn_fwd(&f, to, o_dtype, causal, softmax_scale, nullptr, s_cmp);
+    if (st != SAGE3_OK) break;
+    ck(cudaEventRecord(comp_done[g], s_cmp));
+    ck(cudaStreamWaitEvent(s_out, comp_done[g], 0));
+    ck(cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + h0 * head_out, dout + h0 * head_out, nh * head_out,
+                       cudaMemcpyDeviceToHost, s_out));
+  }
+  // join: the caller's stream waits for everything enqueued above (also on the error path, so that no
+  // library stream is left referencing caller memory unordered)
+  ck(cudaEventRecord(out_done, s_out));
+  cudaStreamWaitEvent(s_cmp, out_done, 0);
+  cudaStreamWaitEvent(s, out_done, 0);
+  cudaEvent_t all[2 * kHostGroups + 2];
+  int k = 0;
+  all[k++] = start;
+  for (int g = 0; g < G; ++g) all[k++] = in_done[g];
+  for (int g = 0; g < G; ++g) all[k++] = comp_done[g];
+  all[k++] = out_done;
+  for (int i = 0; i < n_ev; ++i) cudaEventDestroy(all[i]);  // released once their work completes
   if (st != SAGE3_OK) return st;
-  if ((e = cudaMemcpyAsync(o_host, dout, o_b, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e);
-  return SAGE3_OK;
+  return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
 }
 
 const char* sage3_status_str(sage3_status s) {

@@ -142,3 +142,19 @@ def test_forward_sharded_single_process_matches_direct():
     b = s3.attention(Q, K, V, causal=False)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("B,H,N,d,causal", [(2, 5, 300, 64, False), (1, 11, 1000, 128, True), (1, 1, 128, 128, False)])
+def test_forward_host_pipeline_matches_device_path(B, H, N, d, causal):
+    """sage3_forward_host (head groups pipelined over three streams, pinned host buffers) gives bitwise the
+    device-path result: every (b,h) is an independent problem, so grouping heads cannot change a bit."""
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=99 + H, dtype=torch.bfloat16, device="cuda")
+    want = s3.attention(Q, K, V, causal=causal, out_dtype=torch.bfloat16)
+    qh, kh, vh = (x.cpu().pin_memory() for x in (Q, K, V))
+    oh = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
+    scratch = torch.empty(s3.sage3_forward_host_scratch_bytes(B, H, N, d), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.Stream()
+    s3.sage3_forward_host(qh, kh, vh, oh, scratch, causal=causal, stream=stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(oh, want.cpu())
