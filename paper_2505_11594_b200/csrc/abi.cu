@@ -49,6 +49,11 @@ sage3_status device_ok() {
 
 int esize_of(sage3_dtype t) { return t == SAGE3_FP32 ? 4 : 2; }
 
+// quantize workspace: fp64 K partial sums [B*H][N_pad/128][d], then one u32 arrival counter per head
+size_t partials_bytes(int B, int H, int N, int d) {
+  return ((size_t)B * H * (size_t)(npad(N) / 128) * d * sizeof(double) + 255) & ~size_t(255);
+}
+
 // sage3_forward_host pipeline: head groups and the library-owned streams (one set per device, created on
 // first use, never destroyed: they live as long as the process, like the kernels' attribute setup).
 constexpr int kHostGroups = 8;
@@ -92,7 +97,7 @@ sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]) {
 
 size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d) {
   if (!shape_ok(B, H, N, d)) return 0;
-  return (size_t)B * H * (size_t)(npad(N) / 128) * d * sizeof(double);
+  return partials_bytes(B, H, N, d) + (size_t)B * H * sizeof(uint32_t);
 }
 
 int sage3_kv_tile(int d) { return (d == 64 || d == 128) ? 128 : 0; }
@@ -128,7 +133,8 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   va.H = H, va.N = N, va.Np = out->N_pad, va.d = d;
   va.v_data = out->v_data, va.v_sf = out->v_sf;
   va.nonfinite = nonfinite_flag;
-  cudaError_t e = sage3::launch_quantize(qa, va, in_dtype == SAGE3_BF16, static_cast<double*>(workspace),
+  uint32_t* counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) + partials_bytes(B, H, N, d));
+  cudaError_t e = sage3::launch_quantize(qa, va, in_dtype == SAGE3_BF16, static_cast<double*>(workspace), counters,
                                          static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
 }
@@ -252,8 +258,8 @@ sage3_status sage3_forward_host(const void* q_host, const void* k_host, const vo
     const int64_t sb = (int64_t)nh * N * d;
     sage3_tensor4 tq{dq + h0 * head_in, sb, sh, sn}, tk{dk + h0 * head_in, sb, sh, sn};
     sage3_tensor4 tv{dv + h0 * head_in, sb, sh, sn}, to{dout + h0 * head_out, sb, sh, sn};
-    double* wsg = ws + (size_t)h0 * (Np / 128) * d;
-    st = sage3_quantize_qkv(tq, tk, tv, in_dtype, 1, nh, N, d, &f, wsg, sage3_quantize_workspace_bytes(1, nh, N, d),
+    // groups run in order on the compute stream, so they share one workspace (sized for all heads)
+    st = sage3_quantize_qkv(tq, tk, tv, in_dtype, 1, nh, N, d, &f, ws, sage3_quantize_workspace_bytes(B, H, N, d),
                             nullptr, s_cmp);
     if (st == SAGE3_OK) st = sage3_attn_fwd(&f, to, o_dtype, causal, softmax_scale, nullptr, s_cmp);
     if (st != SAGE3_OK) break;

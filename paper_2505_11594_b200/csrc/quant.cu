@@ -74,167 +74,250 @@ __device__ __forceinline__ bool all_finite(const float* x, int n) {
   return ok;
 }
 
-// ---------------------------------------------------------------------------------- K mean, pass 1
-// grid (Np/128, B*H), block d/2: each thread sums two channels over one 128-token chunk in ascending
-// token order (fp64, sequential), writes ws[bh][chunk][c].
-template <typename T>
-__global__ void __launch_bounds__(64) kmean_partial_kernel(const T* __restrict__ k, int64_t sb, int64_t sh,
-                                                           int64_t sn, int H, int N, int d,
-                                                           double* __restrict__ ws) {
-  const int chunk = blockIdx.x, bh = blockIdx.y;
-  const int b = bh / H, h = bh % H;
-  const int c = threadIdx.x * 2;
-  const T* base = k + b * sb + h * sh + c;
-  const int n0 = chunk * 128, n1 = min(n0 + 128, N);
-  double a0 = 0.0, a1 = 0.0;
-  int n = n0;
-  for (; n + 8 <= n1; n += 8) {
-    uint32_t v[8];
+// ---------------------------------------------------------------------------------- shared pieces
+// Q or K rows of one 128-token chunk: thread t owns row t/2 and G = d/32 consecutive 16-blocks (2G 16-byte
+// loads, 8G code bytes, G scale bytes that are consecutive in the SF atom).  kSmooth: x = fl32(K - km).
+template <typename T, int D, bool kSmooth>
+__device__ __forceinline__ void quant_rows(const T* __restrict__ src, int64_t sn, int N, int n0,
+                                           const float* __restrict__ km, uint8_t* __restrict__ codes_chunk,
+                                           uint8_t* sf_stage, bool& finite) {
+  constexpr int G = D / 32;
+  const int t = threadIdx.x;
+  const int row = t >> 1, g = t & 1;
+  const int n = n0 + row;
+  uint32_t w[2 * G];
+  uint32_t scs = 0;
+  if (n < N) {
+    const T* p = src + (int64_t)n * sn + g * 16 * G;
+    uint4 u[2 * G];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)(n + i) * sn));
+    for (int i = 0; i < 2 * G; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const T* p = reinterpret_cast<const T*>(&v[i]);
-      a0 += (double)to_f32<T>(p[0]);
-      a1 += (double)to_f32<T>(p[1]);
-    }
-  }
-  for (; n < n1; ++n) {
-    uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)n * sn));
-    const T* p = reinterpret_cast<const T*>(&v);
-    a0 += (double)to_f32<T>(p[0]);
-    a1 += (double)to_f32<T>(p[1]);
-  }
-  double* out = ws + ((int64_t)bh * gridDim.x + chunk) * d + c;
-  out[0] = a0;
-  out[1] = a1;
-}
-
-// ---------------------------------------------------------------------------------- K mean, pass 2
-// grid B*H, block d: km = fl32( (Σ_chunks ascending) / N ).
-__global__ void kmean_final_kernel(const double* __restrict__ ws, int nchunks, int N, int d, float* __restrict__ km) {
-  const int bh = blockIdx.x, c = threadIdx.x;
-  const double* p = ws + (int64_t)bh * nchunks * d + c;
-  double total = 0.0;
-  for (int i = 0; i < nchunks; ++i) total += p[(int64_t)i * d];
-  km[(int64_t)bh * d + c] = (float)(total / (double)N);
-}
-
-// ---------------------------------------------------------------------------------- φ of Q and K
-// One thread per (tensor, b, h, n, 16-block); blockIdx.y selects Q (0) or K (1, smoothed).
-template <typename T>
-__global__ void __launch_bounds__(256) quant_qk_kernel(QKArgs a) {
-  const int which = blockIdx.y;
-  const T* src = reinterpret_cast<const T*>(which ? a.k : a.q);
-  const int64_t sb = which ? a.k_sb : a.q_sb, sh = which ? a.k_sh : a.q_sh, sn = which ? a.k_sn : a.q_sn;
-  uint8_t* codes = which ? a.k_data : a.q_data;
-  uint8_t* sf = which ? a.k_sf : a.q_sf;
-  const int C = a.d >> 4;
-  const int64_t total = (int64_t)a.B * a.H * a.Np * C;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int blk = (int)(idx % C);
-  const int64_t row = idx / C;  // bh*Np + n
-  const int n = (int)(row % a.Np);
-  const int bh = (int)(row / a.Np);
-  const int b = bh / a.H, h = bh % a.H;
-  uint32_t lo = 0, hi = 0, sc = 0;
-  if (n < a.N) {
-    const T* p = src + b * sb + h * sh + (int64_t)n * sn + blk * 16;
-    const uint4 u0 = __ldg(reinterpret_cast<const uint4*>(p));
-    const uint4 u1 = __ldg(reinterpret_cast<const uint4*>(p + 8));
-    float x[16];
-    unpack8<T>(u0, x);
-    unpack8<T>(u1, x + 8);
-    if (a.nonfinite && !all_finite(x, 16)) atomicOr(a.nonfinite, 1u);
-    if (which) {
-      const float4* km = reinterpret_cast<const float4*>(a.k_mean + (int64_t)bh * a.d + blk * 16);
+    for (int blk = 0; blk < G; ++blk) {
+      float x[16];
+      unpack8<T>(u[2 * blk], x);
+      unpack8<T>(u[2 * blk + 1], x + 8);
+      finite &= all_finite(x, 16);
+      if constexpr (kSmooth) {
+        const float4* m = reinterpret_cast<const float4*>(km + (g * G + blk) * 16);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 m = km[i];
-        x[4 * i + 0] = __fsub_rn(x[4 * i + 0], m.x);
-        x[4 * i + 1] = __fsub_rn(x[4 * i + 1], m.y);
-        x[4 * i + 2] = __fsub_rn(x[4 * i + 2], m.z);
-        x[4 * i + 3] = __fsub_rn(x[4 * i + 3], m.w);
+        for (int i = 0; i < 4; ++i) {
+          const float4 mm = m[i];
+          x[4 * i + 0] = __fsub_rn(x[4 * i + 0], mm.x);
+          x[4 * i + 1] = __fsub_rn(x[4 * i + 1], mm.y);
+          x[4 * i + 2] = __fsub_rn(x[4 * i + 2], mm.z);
+          x[4 * i + 3] = __fsub_rn(x[4 * i + 3], mm.w);
+        }
       }
+      uint32_t sc;
+      phi16(x, w[2 * blk], w[2 * blk + 1], sc);
+      scs |= sc << (8 * blk);
     }
-    phi16(x, lo, hi, sc);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2 * G; ++i) w[i] = 0u;
   }
-  *reinterpret_cast<uint2*>(codes + row * (a.d >> 1) + blk * 8) = make_uint2(lo, hi);
-  sf[(int64_t)bh * a.Np * C + sf_offset(n, blk, C)] = (uint8_t)sc;
+  // codes: row-major, D/2 bytes per row -> this thread's 8G bytes are contiguous and consecutive threads
+  // are consecutive (fully coalesced 16-byte stores)
+  uint4* dst = reinterpret_cast<uint4*>(codes_chunk + row * (D / 2) + g * 8 * G);
+#pragma unroll
+  for (int i = 0; i < G / 2; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+  // scales: block columns g*G .. g*G+G-1 of row `row` are consecutive bytes of one 512-byte atom
+  const int c0 = g * G;
+  const int off = (c0 >> 2) * 512 + (row & 31) * 16 + ((row >> 5) & 3) * 4 + (c0 & 3);
+  if constexpr (G == 4)
+    *reinterpret_cast<uint32_t*>(sf_stage + off) = scs;
+  else
+    *reinterpret_cast<uint16_t*>(sf_stage + off) = (uint16_t)scs;
 }
 
-// ---------------------------------------------------------------------------------- φ of V^T
-// grid (Np/128, B*H), block 256.  Stage a 128-token x d tile in smem (coalesced 16-byte loads), then each
-// thread quantizes (channel, 16-token block) pairs and writes V^T codes / SF atoms.  Channel rows
-// d..127 of the SF matrix are written as zero (the MMA reads 128 rows of scales).
-template <typename T>
-__global__ void __launch_bounds__(256) quant_v_kernel(VArgs a) {
-  __shared__ __align__(16) T tile[128 * 128];
+// Copy `bytes` (multiple of 16) from smem to global with 16-byte stores by the whole block.
+__device__ __forceinline__ void block_copy16(uint8_t* __restrict__ gdst, const uint8_t* sdst, int bytes) {
+  for (int i = threadIdx.x * 16; i < bytes; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(gdst + i) = *reinterpret_cast<const uint4*>(sdst + i);
+}
+
+// ---------------------------------------------------------------------------------- pass A: Q, V, ΣK
+// grid (Np/128, B*H), block 256, one 128-token chunk of one (b,h):
+//   φ(Q) rows (along d); φ(Vᵀ) (16-token blocks per channel, via an smem transpose, staged codes and SF
+//   atoms written with coalesced 16-byte stores); fp64 per-channel sums of the K chunk (sequential in token
+//   order, c10) into ws.  The last chunk CTA of a head (atomic counter) then reduces the chunk sums in
+//   ascending chunk order and writes km = fl32(total / N); pass B (φ(K - km)) runs after it in stream order.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) quant_pass_a_kernel(QKArgs qa, VArgs va, double* __restrict__ ws,
+                                                           uint32_t* __restrict__ counters) {
+  constexpr int kVec = D / 8;  // 16-byte vectors per token row
+  extern __shared__ __align__(16) uint8_t dsm[];
+  T* sK = reinterpret_cast<T*>(dsm);                                 // K chunk [128][D]
+  T* sV = sK + 128 * D;                                               // V chunk [128][D]
+  uint8_t* sVcode = reinterpret_cast<uint8_t*>(sV + 128 * D);         // Vᵀ codes: D channel rows x 64 bytes
+  uint8_t(*sSF)[1024] = reinterpret_cast<uint8_t(*)[1024]>(sVcode + D * 64);  // [0] Q SF, [1] Vᵀ SF atoms
+  __shared__ uint32_t s_last;
   const int chunk = blockIdx.x, bh = blockIdx.y;
-  const int b = bh / a.H, h = bh % a.H;
-  const int d = a.d;
-  const int vec_per_row = d / 8;
-  const T* base = reinterpret_cast<const T*>(a.v) + b * a.sb + h * a.sh;
+  const int b = bh / qa.H, h = bh % qa.H;
+  const int n0 = chunk * 128, N = qa.N, Np = qa.Np;
+  const int t = threadIdx.x;
   bool finite = true;
-  for (int i = threadIdx.x; i < 128 * vec_per_row; i += blockDim.x) {
-    const int t = i / vec_per_row, cv = i % vec_per_row;
-    const int n = chunk * 128 + t;
-    uint4 u = make_uint4(0, 0, 0, 0);
-    if (n < a.N) {
-      u = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)n * a.sn + cv * 8));
-      if (a.nonfinite) {
+  // ---- stage K and V chunks in smem (16-byte loads, all issued before use)
+  {
+    const T* kb = reinterpret_cast<const T*>(qa.k) + b * qa.k_sb + h * qa.k_sh;
+    const T* vb = reinterpret_cast<const T*>(va.v) + b * va.sb + h * va.sh;
+    constexpr int kIters = 128 * kVec / 256;
+    uint4 uk[kIters], uv[kIters];
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      const int i = it * 256 + t, r = i / kVec, cv = i % kVec, n = n0 + r;
+      uk[it] = n < N ? __ldg(reinterpret_cast<const uint4*>(kb + (int64_t)n * qa.k_sn + cv * 8)) : make_uint4(0, 0, 0, 0);
+      uv[it] = n < N ? __ldg(reinterpret_cast<const uint4*>(vb + (int64_t)n * va.sn + cv * 8)) : make_uint4(0, 0, 0, 0);
+    }
+    // Q rows meanwhile (their loads are in flight with the K/V ones)
+    const T* qb = reinterpret_cast<const T*>(qa.q) + b * qa.q_sb + h * qa.q_sh;
+    for (int i = t; i < 2 * 1024 / 16; i += 256) reinterpret_cast<uint4*>(sSF)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    quant_rows<T, D, false>(qb, qa.q_sn, N, n0, nullptr, qa.q_data + ((int64_t)bh * Np + n0) * (D / 2), sSF[0],
+                            finite);
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      const int i = it * 256 + t;
+      reinterpret_cast<uint4*>(sK)[i] = uk[it];
+      reinterpret_cast<uint4*>(sV)[i] = uv[it];
+      if (qa.nonfinite) {
         float f[8];
-        unpack8<T>(u, f);
+        unpack8<T>(uk[it], f);
+        finite &= all_finite(f, 8);
+        unpack8<T>(uv[it], f);
         finite &= all_finite(f, 8);
       }
     }
-    *reinterpret_cast<uint4*>(&tile[t * d + cv * 8]) = u;
   }
-  if (!finite) atomicOr(a.nonfinite, 1u);
   __syncthreads();
-  const int Cv = a.Np >> 4;
-  uint8_t* sf = a.v_sf + (int64_t)bh * 128 * Cv;
-  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x) {
-    const int tb = i & 7, c = i >> 3;
-    const int tbg = chunk * 8 + tb;
-    uint32_t lo = 0, hi = 0, sc = 0;
-    if (c < d) {
-      float x[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) x[k] = to_f32<T>(tile[(tb * 16 + k) * d + c]);
-      phi16(x, lo, hi, sc);
-      *reinterpret_cast<uint2*>(a.v_data + ((int64_t)bh * d + c) * (a.Np >> 1) + tbg * 8) = make_uint2(lo, hi);
+  // ---- ΣK over the chunk's real tokens, fp64, ascending token order: threads 0..D/2-1, two channels each
+  if (t < D / 2) {
+    const int nend = min(128, N - n0);
+    double a0 = 0.0, a1 = 0.0;
+    const uint32_t* col = reinterpret_cast<const uint32_t*>(sK) + t;
+    for (int r = 0; r < nend; ++r) {
+      const uint32_t u = col[r * (D / 2)];
+      const T* p = reinterpret_cast<const T*>(&u);
+      a0 += (double)to_f32<T>(p[0]);
+      a1 += (double)to_f32<T>(p[1]);
     }
-    sf[sf_offset(c, tbg, Cv)] = (uint8_t)sc;
+    double* out = ws + ((int64_t)bh * gridDim.x + chunk) * D + 2 * t;
+    out[0] = a0;
+    out[1] = a1;
   }
+  // ---- φ(Vᵀ): item = (channel pair cp, 16-token block tb); consecutive threads read consecutive 32-bit
+  //      words of a token row (conflict-free), 16 token rows per block
+  for (int item = t; item < (D / 2) * 8; item += 256) {
+    const int cp = item % (D / 2), tb = item / (D / 2);
+    float x0[16], x1[16];
+    const uint32_t* col = reinterpret_cast<const uint32_t*>(sV) + tb * 16 * (D / 2) + cp;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t u = col[k * (D / 2)];
+      const T* p = reinterpret_cast<const T*>(&u);
+      x0[k] = to_f32<T>(p[0]);
+      x1[k] = to_f32<T>(p[1]);
+    }
+    uint32_t lo, hi, sc0, sc1;
+    const int c = 2 * cp;
+    phi16(x0, lo, hi, sc0);
+    *reinterpret_cast<uint2*>(sVcode + c * 64 + tb * 8) = make_uint2(lo, hi);
+    phi16(x1, lo, hi, sc1);
+    *reinterpret_cast<uint2*>(sVcode + (c + 1) * 64 + tb * 8) = make_uint2(lo, hi);
+    const int base = (tb >> 2) * 512 + ((c >> 5) & 3) * 4 + (tb & 3);
+    sSF[1][base + (c & 31) * 16] = (uint8_t)sc0;
+    sSF[1][base + ((c + 1) & 31) * 16] = (uint8_t)sc1;
+  }
+  if (qa.nonfinite && !finite) atomicOr(qa.nonfinite, 1u);
+  __syncthreads();
+  // ---- coalesced stores: Vᵀ code rows (64 bytes of channel c per chunk), Q and Vᵀ SF atoms
+  for (int i = t; i < D * 4; i += 256) {
+    const int c = i >> 2, q = i & 3;
+    *reinterpret_cast<uint4*>(va.v_data + ((int64_t)bh * D + c) * (Np >> 1) + chunk * 64 + q * 16) =
+        *reinterpret_cast<const uint4*>(sVcode + c * 64 + q * 16);
+  }
+  block_copy16(qa.q_sf + (int64_t)bh * Np * (D / 16) + (int64_t)chunk * 512 * (D / 64), sSF[0], 512 * (D / 64));
+  block_copy16(va.v_sf + (int64_t)bh * 128 * (Np >> 4) + (int64_t)chunk * 1024, sSF[1], 1024);
+  // ---- last chunk CTA of this head: km = fl32(Σ_chunks (ascending) / N)
+  __threadfence();
+  __syncthreads();
+  if (t == 0) s_last = atomicAdd(&counters[bh], 1u) == gridDim.x - 1 ? 1u : 0u;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int nch = gridDim.x;
+    for (int c = t; c < D; c += 256) {
+      const double* p = ws + (int64_t)bh * nch * D + c;
+      double total = 0.0;
+      int i = 0;
+      for (; i + 8 <= nch; i += 8) {  // loads issued together, added in order
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldcg(p + (int64_t)(i + k) * D);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) total += v[k];
+      }
+      for (; i < nch; ++i) total += __ldcg(p + (int64_t)i * D);
+      qa.k_mean[(int64_t)bh * D + c] = (float)(total / (double)N);
+    }
+    if (t == 0) counters[bh] = 0u;  // ready for the next call (also zeroed by the host before pass A)
+  }
+}
+
+// ---------------------------------------------------------------------------------- pass B: φ(K - km)
+template <typename T, int D>
+__global__ void __launch_bounds__(256) quant_pass_b_kernel(QKArgs qa) {
+  __shared__ __align__(16) uint8_t sSF[1024];
+  __shared__ __align__(16) float sKm[D];
+  const int chunk = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / qa.H, h = bh % qa.H;
+  const int t = threadIdx.x;
+  for (int i = t; i < 1024 / 16; i += 256) reinterpret_cast<uint4*>(sSF)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = t; i < D; i += 256) sKm[i] = qa.k_mean[(int64_t)bh * D + i];
+  __syncthreads();
+  bool finite = true;
+  const T* kb = reinterpret_cast<const T*>(qa.k) + b * qa.k_sb + h * qa.k_sh;
+  quant_rows<T, D, true>(kb, qa.k_sn, qa.N, chunk * 128, sKm, qa.k_data + ((int64_t)bh * qa.Np + chunk * 128) * (D / 2),
+                         sSF, finite);
+  __syncthreads();
+  block_copy16(qa.k_sf + (int64_t)bh * qa.Np * (D / 16) + (int64_t)chunk * 512 * (D / 64), sSF, 512 * (D / 64));
+}
+
+template <int D>
+constexpr int pass_a_smem() {
+  return 2 * 128 * D * 2 + D * 64 + 2 * 1024;
+}
+
+template <typename T, int D>
+cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, uint32_t* counters, cudaStream_t stream) {
+  static bool attr_done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(quant_pass_a_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         pass_a_smem<D>());
+    if (e != cudaSuccess) return e;
+    attr_done[dev] = true;
+  }
+  const int BH = qk.B * qk.H;
+  dim3 grid(qk.Np / 128, BH);
+  quant_pass_a_kernel<T, D><<<grid, 256, pass_a_smem<D>(), stream>>>(qk, v, ws, counters);
+  quant_pass_b_kernel<T, D><<<grid, 256, 0, stream>>>(qk);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream) {
-  const int BH = qk.B * qk.H;
-  const int nchunks = qk.Np / 128;
-  dim3 g1(nchunks, BH);
-  if (bf16)
-    kmean_partial_kernel<__nv_bfloat16><<<g1, qk.d / 2, 0, stream>>>(
-        reinterpret_cast<const __nv_bfloat16*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn, qk.H, qk.N, qk.d, ws);
-  else
-    kmean_partial_kernel<__half><<<g1, qk.d / 2, 0, stream>>>(reinterpret_cast<const __half*>(qk.k), qk.k_sb,
-                                                              qk.k_sh, qk.k_sn, qk.H, qk.N, qk.d, ws);
-  kmean_final_kernel<<<BH, qk.d, 0, stream>>>(ws, nchunks, qk.N, qk.d, qk.k_mean);
-  const int64_t total = (int64_t)BH * qk.Np * (qk.d / 16);
-  dim3 g2((unsigned)((total + 255) / 256), 2);
-  if (bf16)
-    quant_qk_kernel<__nv_bfloat16><<<g2, 256, 0, stream>>>(qk);
-  else
-    quant_qk_kernel<__half><<<g2, 256, 0, stream>>>(qk);
-  dim3 g3(nchunks, BH);
-  if (bf16)
-    quant_v_kernel<__nv_bfloat16><<<g3, 256, 0, stream>>>(v);
-  else
-    quant_v_kernel<__half><<<g3, 256, 0, stream>>>(v);
-  return cudaGetLastError();
+cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, uint32_t* counters,
+                            cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(uint32_t) * qk.B * qk.H, stream);
+  if (e != cudaSuccess) return e;
+  if (qk.d == 128)
+    return bf16 ? launch_t<__nv_bfloat16, 128>(qk, v, ws, counters, stream)
+                : launch_t<__half, 128>(qk, v, ws, counters, stream);
+  return bf16 ? launch_t<__nv_bfloat16, 64>(qk, v, ws, counters, stream)
+              : launch_t<__half, 64>(qk, v, ws, counters, stream);
 }
 
 }  // namespace sage3
