@@ -80,8 +80,7 @@ typedef struct {
  * k_mean.  Returns SAGE3_ERR_INVALID_ARG for unsupported shapes. */
 sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]);
 
-/* Device workspace of sage3_quantize_qkv: fp64 K-mean partial sums (B*H*(N_pad/128)*d*8 bytes, rounded up
- * to 256) followed by one u32 per head (arrival counters, zeroed by the call itself). */
+/* Device workspace of sage3_quantize_qkv: fp64 K-mean partial sums, B*H*(N_pad/128)*d*8 bytes. */
 size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d);
 
 /* B_kv (keys per tile) used by sage3_attn_fwd for head dim d.  The per-tile first-level P scale s_P1

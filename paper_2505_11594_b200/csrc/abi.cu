@@ -49,11 +49,6 @@ sage3_status device_ok() {
 
 int esize_of(sage3_dtype t) { return t == SAGE3_FP32 ? 4 : 2; }
 
-// quantize workspace: fp64 K partial sums [B*H][N_pad/128][d], then one u32 arrival counter per head
-size_t partials_bytes(int B, int H, int N, int d) {
-  return ((size_t)B * H * (size_t)(npad(N) / 128) * d * sizeof(double) + 255) & ~size_t(255);
-}
-
 // sage3_forward_host pipeline: head groups and the library-owned streams (one set per device, created on
 // first use, never destroyed: they live as long as the process, like the kernels' attribute setup).
 constexpr int kHostGroups = 8;
@@ -97,7 +92,7 @@ sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]) {
 
 size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d) {
   if (!shape_ok(B, H, N, d)) return 0;
-  return partials_bytes(B, H, N, d) + (size_t)B * H * sizeof(uint32_t);
+  return (size_t)B * H * (size_t)(npad(N) / 128) * d * sizeof(double);
 }
 
 int sage3_kv_tile(int d) { return (d == 64 || d == 128) ? 128 : 0; }
@@ -133,8 +128,7 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   va.H = H, va.N = N, va.Np = out->N_pad, va.d = d;
   va.v_data = out->v_data, va.v_sf = out->v_sf;
   va.nonfinite = nonfinite_flag;
-  uint32_t* counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) + partials_bytes(B, H, N, d));
-  cudaError_t e = sage3::launch_quantize(qa, va, in_dtype == SAGE3_BF16, static_cast<double*>(workspace), counters,
+  cudaError_t e = sage3::launch_quantize(qa, va, in_dtype == SAGE3_BF16, static_cast<double*>(workspace),
                                          static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
 }

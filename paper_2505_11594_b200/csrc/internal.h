@@ -26,8 +26,7 @@ struct VArgs {
 };
 
 // k_mean is QKArgs::k_mean (non-const alias for the writer).
-cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, uint32_t* counters,
-                            cudaStream_t stream);
+cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream);
 
 struct AttnArgs {
   const uint8_t *q_data, *k_data, *v_data, *q_sf, *k_sf, *v_sf;

@@ -75,60 +75,56 @@ __device__ __forceinline__ bool all_finite(const float* x, int n) {
 }
 
 // ---------------------------------------------------------------------------------- shared pieces
-// Q or K rows of one 128-token chunk: thread t owns row t/2 and G = d/32 consecutive 16-blocks (2G 16-byte
-// loads, 8G code bytes, G scale bytes that are consecutive in the SF atom).  kSmooth: x = fl32(K - km).
+// Q or K rows of one 128-token chunk (φ along d).  The chunk is read as consecutive 16-byte vectors (vector
+// i = it*256 + t: every warp load instruction covers 512 contiguous bytes); the two threads holding the two
+// halves of a 16-element block exchange their partial amax with one shuffle and each writes the 4 code bytes
+// of its half (again consecutive across the warp).  Scale bytes go to the chunk's SF atoms staged in smem.
+// kSmooth: x = fl32(K - km).
 template <typename T, int D, bool kSmooth>
 __device__ __forceinline__ void quant_rows(const T* __restrict__ src, int64_t sn, int N, int n0,
                                            const float* __restrict__ km, uint8_t* __restrict__ codes_chunk,
                                            uint8_t* sf_stage, bool& finite) {
-  constexpr int G = D / 32;
+  constexpr int kVec = D / 8;              // 16-byte vectors per row
+  constexpr int kIt = 128 * kVec / 256;    // vectors per thread
   const int t = threadIdx.x;
-  const int row = t >> 1, g = t & 1;
-  const int n = n0 + row;
-  uint32_t w[2 * G];
-  uint32_t scs = 0;
-  if (n < N) {
-    const T* p = src + (int64_t)n * sn + g * 16 * G;
-    uint4 u[2 * G];
+  uint4 u[kIt];
 #pragma unroll
-    for (int i = 0; i < 2 * G; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
-#pragma unroll
-    for (int blk = 0; blk < G; ++blk) {
-      float x[16];
-      unpack8<T>(u[2 * blk], x);
-      unpack8<T>(u[2 * blk + 1], x + 8);
-      finite &= all_finite(x, 16);
-      if constexpr (kSmooth) {
-        const float4* m = reinterpret_cast<const float4*>(km + (g * G + blk) * 16);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 mm = m[i];
-          x[4 * i + 0] = __fsub_rn(x[4 * i + 0], mm.x);
-          x[4 * i + 1] = __fsub_rn(x[4 * i + 1], mm.y);
-          x[4 * i + 2] = __fsub_rn(x[4 * i + 2], mm.z);
-          x[4 * i + 3] = __fsub_rn(x[4 * i + 3], mm.w);
-        }
-      }
-      uint32_t sc;
-      phi16(x, w[2 * blk], w[2 * blk + 1], sc);
-      scs |= sc << (8 * blk);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 2 * G; ++i) w[i] = 0u;
+  for (int it = 0; it < kIt; ++it) {
+    const int i = it * 256 + t, r = i / kVec, cv = i % kVec, n = n0 + r;
+    u[it] = n < N ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)n * sn + cv * 8)) : make_uint4(0, 0, 0, 0);
   }
-  // codes: row-major, D/2 bytes per row -> this thread's 8G bytes are contiguous and consecutive threads
-  // are consecutive (fully coalesced 16-byte stores)
-  uint4* dst = reinterpret_cast<uint4*>(codes_chunk + row * (D / 2) + g * 8 * G);
 #pragma unroll
-  for (int i = 0; i < G / 2; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-  // scales: block columns g*G .. g*G+G-1 of row `row` are consecutive bytes of one 512-byte atom
-  const int c0 = g * G;
-  const int off = (c0 >> 2) * 512 + (row & 31) * 16 + ((row >> 5) & 3) * 4 + (c0 & 3);
-  if constexpr (G == 4)
-    *reinterpret_cast<uint32_t*>(sf_stage + off) = scs;
-  else
-    *reinterpret_cast<uint16_t*>(sf_stage + off) = (uint16_t)scs;
+  for (int it = 0; it < kIt; ++it) {
+    const int i = it * 256 + t, r = i / kVec, cv = i % kVec;
+    float x[8];
+    unpack8<T>(u[it], x);
+    finite &= all_finite(x, 8);
+    if constexpr (kSmooth) {
+      const float4 m0 = reinterpret_cast<const float4*>(km + cv * 8)[0];
+      const float4 m1 = reinterpret_cast<const float4*>(km + cv * 8)[1];
+      x[0] = __fsub_rn(x[0], m0.x), x[1] = __fsub_rn(x[1], m0.y), x[2] = __fsub_rn(x[2], m0.z);
+      x[3] = __fsub_rn(x[3], m0.w), x[4] = __fsub_rn(x[4], m1.x), x[5] = __fsub_rn(x[5], m1.y);
+      x[6] = __fsub_rn(x[6], m1.z), x[7] = __fsub_rn(x[7], m1.w);
+    }
+    float amax = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) amax = fmaxf(amax, fabsf(x[k]));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+    const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
+    const float s = e4m3_to_f32(sc);
+    uint32_t w = 0u;
+    if (s != 0.0f) {
+      const float rs = __frcp_rn(s);
+      w = cvt_e2m1x2(__fmul_rn(x[0], rs), __fmul_rn(x[1], rs)) | (cvt_e2m1x2(__fmul_rn(x[2], rs), __fmul_rn(x[3], rs)) << 8) |
+          (cvt_e2m1x2(__fmul_rn(x[4], rs), __fmul_rn(x[5], rs)) << 16) |
+          (cvt_e2m1x2(__fmul_rn(x[6], rs), __fmul_rn(x[7], rs)) << 24);
+    }
+    *reinterpret_cast<uint32_t*>(codes_chunk + r * (D / 2) + cv * 4) = w;
+    if ((cv & 1) == 0) {
+      const int c = cv >> 1;  // block column
+      sf_stage[(c >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (c & 3)] = (uint8_t)sc;
+    }
+  }
 }
 
 // Copy `bytes` (multiple of 16) from smem to global with 16-byte stores by the whole block.
@@ -137,77 +133,106 @@ __device__ __forceinline__ void block_copy16(uint8_t* __restrict__ gdst, const u
     *reinterpret_cast<uint4*>(gdst + i) = *reinterpret_cast<const uint4*>(sdst + i);
 }
 
-// ---------------------------------------------------------------------------------- pass A: Q, V, ΣK
-// grid (Np/128, B*H), block 256, one 128-token chunk of one (b,h):
-//   φ(Q) rows (along d); φ(Vᵀ) (16-token blocks per channel, via an smem transpose, staged codes and SF
-//   atoms written with coalesced 16-byte stores); fp64 per-channel sums of the K chunk (sequential in token
-//   order, c10) into ws.  The last chunk CTA of a head (atomic counter) then reduces the chunk sums in
-//   ascending chunk order and writes km = fl32(total / N); pass B (φ(K - km)) runs after it in stream order.
+// ---------------------------------------------------------------------------------- K mean
+// grid (Np/128, B*H), block d/2: thread t sums channels 2t, 2t+1 over one 128-token chunk in ascending token
+// order (fp64, sequential; 4-byte loads, a warp reads 128 contiguous bytes of a token row), writes
+// ws[bh][chunk][c]; kmean_final_kernel then reduces the chunk sums (reading c10).
+template <typename T>
+__global__ void __launch_bounds__(64) kmean_kernel(const T* __restrict__ k, int64_t sb, int64_t sh, int64_t sn,
+                                                   int H, int N, int d, double* __restrict__ ws) {
+  const int chunk = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int c = threadIdx.x * 2;
+  const T* base = k + b * sb + h * sh + c;
+  const int n0 = chunk * 128, n1 = min(n0 + 128, N);
+  double a0 = 0.0, a1 = 0.0;
+  int n = n0;
+  for (; n + 8 <= n1; n += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)(n + i) * sn));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const T* p = reinterpret_cast<const T*>(&v[i]);
+      a0 += (double)to_f32<T>(p[0]);
+      a1 += (double)to_f32<T>(p[1]);
+    }
+  }
+  for (; n < n1; ++n) {
+    const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)n * sn));
+    const T* p = reinterpret_cast<const T*>(&v);
+    a0 += (double)to_f32<T>(p[0]);
+    a1 += (double)to_f32<T>(p[1]);
+  }
+  double* out = ws + ((int64_t)bh * gridDim.x + chunk) * d + c;
+  out[0] = a0;
+  out[1] = a1;
+}
+
+// grid (B*H*d/128), block 128: one thread per (bh, channel) sums the chunk sums in ascending chunk order
+// (loads issued 8 at a time, added in order) and writes km = fl32(total / N).
+__global__ void __launch_bounds__(128) kmean_final_kernel(const double* __restrict__ ws, int nchunks, int N, int d,
+                                                          int total_ch, float* __restrict__ km) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total_ch) return;
+  const int bh = idx / d, c = idx % d;
+  const double* p = ws + (int64_t)bh * nchunks * d + c;
+  double total = 0.0;
+  int i = 0;
+  for (; i + 8 <= nchunks; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = p[(int64_t)(i + q) * d];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) total += v[q];
+  }
+  for (; i < nchunks; ++i) total += p[(int64_t)i * d];
+  km[idx] = (float)(total / (double)N);
+}
+
+// ---------------------------------------------------------------------------------- Q and Vᵀ
+// grid (Np/128, B*H), block 256, one 128-token chunk of one (b,h): φ(Q) rows (along d) straight from
+// registers; φ(Vᵀ) (16-token blocks per channel) through an smem transpose, codes and SF atoms staged in
+// smem and written with coalesced 16-byte stores.
 template <typename T, int D>
-__global__ void __launch_bounds__(256) quant_pass_a_kernel(QKArgs qa, VArgs va, double* __restrict__ ws,
-                                                           uint32_t* __restrict__ counters) {
+__global__ void __launch_bounds__(256) quant_qv_kernel(QKArgs qa, VArgs va) {
   constexpr int kVec = D / 8;  // 16-byte vectors per token row
   extern __shared__ __align__(16) uint8_t dsm[];
-  T* sK = reinterpret_cast<T*>(dsm);                                 // K chunk [128][D]
-  T* sV = sK + 128 * D;                                               // V chunk [128][D]
+  T* sV = reinterpret_cast<T*>(dsm);                                  // V chunk [128][D]
   uint8_t* sVcode = reinterpret_cast<uint8_t*>(sV + 128 * D);         // Vᵀ codes: D channel rows x 64 bytes
   uint8_t(*sSF)[1024] = reinterpret_cast<uint8_t(*)[1024]>(sVcode + D * 64);  // [0] Q SF, [1] Vᵀ SF atoms
-  __shared__ uint32_t s_last;
   const int chunk = blockIdx.x, bh = blockIdx.y;
   const int b = bh / qa.H, h = bh % qa.H;
   const int n0 = chunk * 128, N = qa.N, Np = qa.Np;
   const int t = threadIdx.x;
   bool finite = true;
-  // ---- stage K and V chunks in smem (16-byte loads, all issued before use)
   {
-    const T* kb = reinterpret_cast<const T*>(qa.k) + b * qa.k_sb + h * qa.k_sh;
     const T* vb = reinterpret_cast<const T*>(va.v) + b * va.sb + h * va.sh;
     constexpr int kIters = 128 * kVec / 256;
-    uint4 uk[kIters], uv[kIters];
+    uint4 uv[kIters];
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
       const int i = it * 256 + t, r = i / kVec, cv = i % kVec, n = n0 + r;
-      uk[it] = n < N ? __ldg(reinterpret_cast<const uint4*>(kb + (int64_t)n * qa.k_sn + cv * 8)) : make_uint4(0, 0, 0, 0);
       uv[it] = n < N ? __ldg(reinterpret_cast<const uint4*>(vb + (int64_t)n * va.sn + cv * 8)) : make_uint4(0, 0, 0, 0);
     }
-    // Q rows meanwhile (their loads are in flight with the K/V ones)
-    const T* qb = reinterpret_cast<const T*>(qa.q) + b * qa.q_sb + h * qa.q_sh;
     for (int i = t; i < 2 * 1024 / 16; i += 256) reinterpret_cast<uint4*>(sSF)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
+    const T* qb = reinterpret_cast<const T*>(qa.q) + b * qa.q_sb + h * qa.q_sh;
     quant_rows<T, D, false>(qb, qa.q_sn, N, n0, nullptr, qa.q_data + ((int64_t)bh * Np + n0) * (D / 2), sSF[0],
                             finite);
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
-      const int i = it * 256 + t;
-      reinterpret_cast<uint4*>(sK)[i] = uk[it];
-      reinterpret_cast<uint4*>(sV)[i] = uv[it];
+      reinterpret_cast<uint4*>(sV)[it * 256 + t] = uv[it];
       if (qa.nonfinite) {
         float f[8];
-        unpack8<T>(uk[it], f);
-        finite &= all_finite(f, 8);
         unpack8<T>(uv[it], f);
         finite &= all_finite(f, 8);
       }
     }
   }
   __syncthreads();
-  // ---- ΣK over the chunk's real tokens, fp64, ascending token order: threads 0..D/2-1, two channels each
-  if (t < D / 2) {
-    const int nend = min(128, N - n0);
-    double a0 = 0.0, a1 = 0.0;
-    const uint32_t* col = reinterpret_cast<const uint32_t*>(sK) + t;
-    for (int r = 0; r < nend; ++r) {
-      const uint32_t u = col[r * (D / 2)];
-      const T* p = reinterpret_cast<const T*>(&u);
-      a0 += (double)to_f32<T>(p[0]);
-      a1 += (double)to_f32<T>(p[1]);
-    }
-    double* out = ws + ((int64_t)bh * gridDim.x + chunk) * D + 2 * t;
-    out[0] = a0;
-    out[1] = a1;
-  }
-  // ---- φ(Vᵀ): item = (channel pair cp, 16-token block tb); consecutive threads read consecutive 32-bit
-  //      words of a token row (conflict-free), 16 token rows per block
+  // item = (channel pair cp, 16-token block tb); consecutive threads read consecutive 32-bit words of a
+  // token row (conflict-free), 16 token rows per block
   for (int item = t; item < (D / 2) * 8; item += 256) {
     const int cp = item % (D / 2), tb = item / (D / 2);
     float x0[16], x1[16];
@@ -231,7 +256,6 @@ __global__ void __launch_bounds__(256) quant_pass_a_kernel(QKArgs qa, VArgs va, 
   }
   if (qa.nonfinite && !finite) atomicOr(qa.nonfinite, 1u);
   __syncthreads();
-  // ---- coalesced stores: Vᵀ code rows (64 bytes of channel c per chunk), Q and Vᵀ SF atoms
   for (int i = t; i < D * 4; i += 256) {
     const int c = i >> 2, q = i & 3;
     *reinterpret_cast<uint4*>(va.v_data + ((int64_t)bh * D + c) * (Np >> 1) + chunk * 64 + q * 16) =
@@ -239,30 +263,6 @@ __global__ void __launch_bounds__(256) quant_pass_a_kernel(QKArgs qa, VArgs va, 
   }
   block_copy16(qa.q_sf + (int64_t)bh * Np * (D / 16) + (int64_t)chunk * 512 * (D / 64), sSF[0], 512 * (D / 64));
   block_copy16(va.v_sf + (int64_t)bh * 128 * (Np >> 4) + (int64_t)chunk * 1024, sSF[1], 1024);
-  // ---- last chunk CTA of this head: km = fl32(Σ_chunks (ascending) / N)
-  __threadfence();
-  __syncthreads();
-  if (t == 0) s_last = atomicAdd(&counters[bh], 1u) == gridDim.x - 1 ? 1u : 0u;
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    const int nch = gridDim.x;
-    for (int c = t; c < D; c += 256) {
-      const double* p = ws + (int64_t)bh * nch * D + c;
-      double total = 0.0;
-      int i = 0;
-      for (; i + 8 <= nch; i += 8) {  // loads issued together, added in order
-        double v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldcg(p + (int64_t)(i + k) * D);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) total += v[k];
-      }
-      for (; i < nch; ++i) total += __ldcg(p + (int64_t)i * D);
-      qa.k_mean[(int64_t)bh * D + c] = (float)(total / (double)N);
-    }
-    if (t == 0) counters[bh] = 0u;  // ready for the next call (also zeroed by the host before pass A)
-  }
 }
 
 // ---------------------------------------------------------------------------------- pass B: φ(K - km)
@@ -285,39 +285,39 @@ __global__ void __launch_bounds__(256) quant_pass_b_kernel(QKArgs qa) {
 }
 
 template <int D>
-constexpr int pass_a_smem() {
-  return 2 * 128 * D * 2 + D * 64 + 2 * 1024;
+constexpr int qv_smem() {
+  return 128 * D * 2 + D * 64 + 2 * 1024;
 }
 
 template <typename T, int D>
-cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, uint32_t* counters, cudaStream_t stream) {
+cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t stream) {
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(quant_pass_a_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         pass_a_smem<D>());
+    cudaError_t e = cudaFuncSetAttribute(quant_qv_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         qv_smem<D>());
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
   const int BH = qk.B * qk.H;
   dim3 grid(qk.Np / 128, BH);
-  quant_pass_a_kernel<T, D><<<grid, 256, pass_a_smem<D>(), stream>>>(qk, v, ws, counters);
+  kmean_kernel<T><<<grid, D / 2, 0, stream>>>(reinterpret_cast<const T*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn, qk.H,
+                                              qk.N, D, ws);
+  kmean_final_kernel<<<(BH * D + 127) / 128, 128, 0, stream>>>(ws, qk.Np / 128, qk.N, D, BH * D, qk.k_mean);
+  quant_qv_kernel<T, D><<<grid, 256, qv_smem<D>(), stream>>>(qk, v);
   quant_pass_b_kernel<T, D><<<grid, 256, 0, stream>>>(qk);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, uint32_t* counters,
-                            cudaStream_t stream) {
-  cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(uint32_t) * qk.B * qk.H, stream);
-  if (e != cudaSuccess) return e;
+cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream) {
   if (qk.d == 128)
-    return bf16 ? launch_t<__nv_bfloat16, 128>(qk, v, ws, counters, stream)
-                : launch_t<__half, 128>(qk, v, ws, counters, stream);
-  return bf16 ? launch_t<__nv_bfloat16, 64>(qk, v, ws, counters, stream)
-              : launch_t<__half, 64>(qk, v, ws, counters, stream);
+    return bf16 ? launch_t<__nv_bfloat16, 128>(qk, v, ws, stream)
+                : launch_t<__half, 128>(qk, v, ws, stream);
+  return bf16 ? launch_t<__nv_bfloat16, 64>(qk, v, ws, stream)
+              : launch_t<__half, 64>(qk, v, ws, stream);
 }
 
 }  // namespace sage3
