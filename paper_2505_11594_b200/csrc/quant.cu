@@ -1,6 +1,7 @@
 // quant.cu — sm_100a kernels for sage3_quantize_qkv: smoothing K (Alg1 L2) and NVFP4
 // microscaling φ (Eq. 1) of Q, K (1x16 blocks along d) and V (1x16 blocks along tokens, written
-// transposed).  HBM-bound streaming kernels: 128-bit loads, one thread per 16-element block.
+// transposed).  HBM-bound: K-mean sums (4-byte coalesced loads, fp64) + their fixed-order reduction,
+// then one persistent streaming kernel (TMA tiles -> smem ring -> φ) over all Q, Vᵀ and K chunks.
 //
 // Numerics are the DESIGN.md §3 readings, implemented with explicitly rounded intrinsics so that no FMA
 // contraction or fast-math can change a bit:
@@ -12,6 +13,9 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <mutex>
+
+#include <cudaTypedefs.h>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -22,6 +26,19 @@ namespace {
 using namespace ptx;
 
 constexpr float kOneSixth = 0x1.555556p-3f;  // fl32(1/6) = 0x3E2AAAAB
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_q() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
 
 template <typename T>
 __device__ __forceinline__ float to_f32(T v);
@@ -42,95 +59,25 @@ __device__ __forceinline__ void unpack8(const uint4& u, float* f) {
   for (int i = 0; i < 8; ++i) f[i] = to_f32<T>(h[i]);
 }
 
-// Byte offset of scale (row r, block-column c) inside one (b,h) SF matrix with C block-columns.
-__device__ __forceinline__ uint32_t sf_offset(uint32_t r, uint32_t c, uint32_t C) {
-  return ((r >> 7) * (C >> 2) + (c >> 2)) * 512u + (r & 31u) * 16u + ((r >> 5) & 3u) * 4u + (c & 3u);
+// max|x| over 8 / 16 values with NaN propagation (FMNMX3.NAN with |.| source modifiers): an infinite or
+// NaN input makes the block amax non-finite, which is how the non-finite flag is detected per block.
+__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
 }
-
-// φ of one 16-element block (already in fp32, exact input values).  Returns 8 packed code bytes (lo word,
-// hi word) and the E4M3 scale code.
-__device__ __forceinline__ void phi16(const float* x, uint32_t& lo, uint32_t& hi, uint32_t& sc) {
-  float amax = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) amax = fmaxf(amax, fabsf(x[i]));
-  const float s32 = __fmul_rn(amax, kOneSixth);
-  sc = cvt_e4m3x2(s32, 0.0f) & 0xFFu;
-  const float s = e4m3_to_f32(sc);
-  if (s == 0.0f) {
-    lo = hi = 0u;
-    return;
-  }
-  const float r = __frcp_rn(s);
-  uint32_t b[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) b[i] = cvt_e2m1x2(__fmul_rn(x[2 * i], r), __fmul_rn(x[2 * i + 1], r));
-  lo = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
-  hi = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
+__device__ __forceinline__ float amax8(const float* x) {
+  const float a = fmax3_nan(fabsf(x[0]), fabsf(x[1]), fabsf(x[2]));
+  const float b = fmax3_nan(fabsf(x[3]), fabsf(x[4]), fabsf(x[5]));
+  return fmax3_nan(a, b, fmax3_nan(fabsf(x[6]), fabsf(x[7]), 0.0f));
 }
-
-__device__ __forceinline__ bool all_finite(const float* x, int n) {
-  bool ok = true;
-  for (int i = 0; i < n; ++i) ok &= isfinite(x[i]);
-  return ok;
-}
-
-// ---------------------------------------------------------------------------------- shared pieces
-// Q or K rows of one 128-token chunk (φ along d).  The chunk is read as consecutive 16-byte vectors (vector
-// i = it*256 + t: every warp load instruction covers 512 contiguous bytes); the two threads holding the two
-// halves of a 16-element block exchange their partial amax with one shuffle and each writes the 4 code bytes
-// of its half (again consecutive across the warp).  Scale bytes go to the chunk's SF atoms staged in smem.
-// kSmooth: x = fl32(K - km).
-template <typename T, int D, bool kSmooth>
-__device__ __forceinline__ void quant_rows(const T* __restrict__ src, int64_t sn, int N, int n0,
-                                           const float* __restrict__ km, uint8_t* __restrict__ codes_chunk,
-                                           uint8_t* sf_stage, bool& finite) {
-  constexpr int kVec = D / 8;              // 16-byte vectors per row
-  constexpr int kIt = 128 * kVec / 256;    // vectors per thread
-  const int t = threadIdx.x;
-  uint4 u[kIt];
-#pragma unroll
-  for (int it = 0; it < kIt; ++it) {
-    const int i = it * 256 + t, r = i / kVec, cv = i % kVec, n = n0 + r;
-    u[it] = n < N ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)n * sn + cv * 8)) : make_uint4(0, 0, 0, 0);
-  }
-#pragma unroll
-  for (int it = 0; it < kIt; ++it) {
-    const int i = it * 256 + t, r = i / kVec, cv = i % kVec;
-    float x[8];
-    unpack8<T>(u[it], x);
-    finite &= all_finite(x, 8);
-    if constexpr (kSmooth) {
-      const float4 m0 = reinterpret_cast<const float4*>(km + cv * 8)[0];
-      const float4 m1 = reinterpret_cast<const float4*>(km + cv * 8)[1];
-      x[0] = __fsub_rn(x[0], m0.x), x[1] = __fsub_rn(x[1], m0.y), x[2] = __fsub_rn(x[2], m0.z);
-      x[3] = __fsub_rn(x[3], m0.w), x[4] = __fsub_rn(x[4], m1.x), x[5] = __fsub_rn(x[5], m1.y);
-      x[6] = __fsub_rn(x[6], m1.z), x[7] = __fsub_rn(x[7], m1.w);
-    }
-    float amax = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) amax = fmaxf(amax, fabsf(x[k]));
-    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-    const uint32_t sc = cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu;
-    const float s = e4m3_to_f32(sc);
-    uint32_t w = 0u;
-    if (s != 0.0f) {
-      const float rs = __frcp_rn(s);
-      w = cvt_e2m1x2(__fmul_rn(x[0], rs), __fmul_rn(x[1], rs)) | (cvt_e2m1x2(__fmul_rn(x[2], rs), __fmul_rn(x[3], rs)) << 8) |
-          (cvt_e2m1x2(__fmul_rn(x[4], rs), __fmul_rn(x[5], rs)) << 16) |
-          (cvt_e2m1x2(__fmul_rn(x[6], rs), __fmul_rn(x[7], rs)) << 24);
-    }
-    *reinterpret_cast<uint32_t*>(codes_chunk + r * (D / 2) + cv * 4) = w;
-    if ((cv & 1) == 0) {
-      const int c = cv >> 1;  // block column
-      sf_stage[(c >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (c & 3)] = (uint8_t)sc;
-    }
-  }
-}
-
-// Copy `bytes` (multiple of 16) from smem to global with 16-byte stores by the whole block.
-__device__ __forceinline__ void block_copy16(uint8_t* __restrict__ gdst, const uint8_t* sdst, int bytes) {
-  for (int i = threadIdx.x * 16; i < bytes; i += blockDim.x * 16)
-    *reinterpret_cast<uint4*>(gdst + i) = *reinterpret_cast<const uint4*>(sdst + i);
+// E2M1 codes of x·rs for 8 values (element 0 in the low nibble): 4 FMUL2 (RN, exact same rounding as the
+// oracle's fl32(x·fl32(1/s))) and 4 converts merged into one word.
+__device__ __forceinline__ uint32_t codes8(const float* x, float rs) {
+  const f2 r2 = make_float2(rs, rs);
+  const f2 y0 = fmul2(make_float2(x[0], x[1]), r2), y1 = fmul2(make_float2(x[2], x[3]), r2);
+  const f2 y2 = fmul2(make_float2(x[4], x[5]), r2), y3 = fmul2(make_float2(x[6], x[7]), r2);
+  return cvt_e2m1x8(y0.x, y0.y, y1.x, y1.y, y2.x, y2.y, y3.x, y3.y);
 }
 
 // ---------------------------------------------------------------------------------- K mean
@@ -164,149 +111,250 @@ __global__ void __launch_bounds__(64) kmean_kernel(const T* __restrict__ k, int6
     a0 += (double)to_f32<T>(p[0]);
     a1 += (double)to_f32<T>(p[1]);
   }
-  double* out = ws + ((int64_t)bh * gridDim.x + chunk) * d + c;
+  double* out = ws + ((int64_t)bh * d + c) * gridDim.x + chunk;  // [bh][channel][chunk]
   out[0] = a0;
-  out[1] = a1;
+  out[gridDim.x] = a1;
 }
 
-// grid (B*H*d/128), block 128: one thread per (bh, channel) sums the chunk sums in ascending chunk order
-// (loads issued 8 at a time, added in order) and writes km = fl32(total / N).
-__global__ void __launch_bounds__(128) kmean_final_kernel(const double* __restrict__ ws, int nchunks, int N, int d,
+// One warp per (bh, channel): lane l loads chunk sums 8l..8l+7 (the channel's sums are contiguous:
+// [bh][channel][chunk]), then every lane adds all of them in ascending chunk order (shuffled out of the
+// owning lane) — the sequential fp64 order of reading c10 — and lane 0 writes km = fl32(total / N).
+__global__ void __launch_bounds__(256) kmean_final_kernel(const double* __restrict__ ws, int nchunks, int N,
                                                           int total_ch, float* __restrict__ km) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total_ch) return;
-  const int bh = idx / d, c = idx % d;
-  const double* p = ws + (int64_t)bh * nchunks * d + c;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= total_ch) return;
+  const double* p = ws + (int64_t)w * nchunks;
   double total = 0.0;
-  int i = 0;
-  for (; i + 8 <= nchunks; i += 8) {
+  for (int base = 0; base < nchunks; base += 256) {
     double v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = p[(int64_t)(i + q) * d];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) total += v[q];
-  }
-  for (; i < nchunks; ++i) total += p[(int64_t)i * d];
-  km[idx] = (float)(total / (double)N);
-}
-
-// ---------------------------------------------------------------------------------- Q and Vᵀ
-// grid (Np/128, B*H), block 256, one 128-token chunk of one (b,h): φ(Q) rows (along d) straight from
-// registers; φ(Vᵀ) (16-token blocks per channel) through an smem transpose, codes and SF atoms staged in
-// smem and written with coalesced 16-byte stores.
-template <typename T, int D>
-__global__ void __launch_bounds__(256) quant_qv_kernel(QKArgs qa, VArgs va) {
-  constexpr int kVec = D / 8;  // 16-byte vectors per token row
-  extern __shared__ __align__(16) uint8_t dsm[];
-  T* sV = reinterpret_cast<T*>(dsm);                                  // V chunk [128][D]
-  uint8_t* sVcode = reinterpret_cast<uint8_t*>(sV + 128 * D);         // Vᵀ codes: D channel rows x 64 bytes
-  uint8_t(*sSF)[1024] = reinterpret_cast<uint8_t(*)[1024]>(sVcode + D * 64);  // [0] Q SF, [1] Vᵀ SF atoms
-  const int chunk = blockIdx.x, bh = blockIdx.y;
-  const int b = bh / qa.H, h = bh % qa.H;
-  const int n0 = chunk * 128, N = qa.N, Np = qa.Np;
-  const int t = threadIdx.x;
-  bool finite = true;
-  {
-    const T* vb = reinterpret_cast<const T*>(va.v) + b * va.sb + h * va.sh;
-    constexpr int kIters = 128 * kVec / 256;
-    uint4 uv[kIters];
-#pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-      const int i = it * 256 + t, r = i / kVec, cv = i % kVec, n = n0 + r;
-      uv[it] = n < N ? __ldg(reinterpret_cast<const uint4*>(vb + (int64_t)n * va.sn + cv * 8)) : make_uint4(0, 0, 0, 0);
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + 8 * lane + k;
+      v[k] = i < nchunks ? p[i] : 0.0;
     }
-    for (int i = t; i < 2 * 1024 / 16; i += 256) reinterpret_cast<uint4*>(sSF)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    const T* qb = reinterpret_cast<const T*>(qa.q) + b * qa.q_sb + h * qa.q_sh;
-    quant_rows<T, D, false>(qb, qa.q_sn, N, n0, nullptr, qa.q_data + ((int64_t)bh * Np + n0) * (D / 2), sSF[0],
-                            finite);
+    const int n = min(256, nchunks - base);
+    for (int src = 0; src < 32 && 8 * src < n; ++src) {
 #pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-      reinterpret_cast<uint4*>(sV)[it * 256 + t] = uv[it];
-      if (qa.nonfinite) {
-        float f[8];
-        unpack8<T>(uv[it], f);
-        finite &= all_finite(f, 8);
+      for (int k = 0; k < 8; ++k) {
+        const double x = __shfl_sync(0xffffffffu, v[k], src);
+        if (8 * src + k < n) total += x;
       }
     }
   }
-  __syncthreads();
-  // item = (channel pair cp, 16-token block tb); consecutive threads read consecutive 32-bit words of a
-  // token row (conflict-free), 16 token rows per block
-  for (int item = t; item < (D / 2) * 8; item += 256) {
-    const int cp = item % (D / 2), tb = item / (D / 2);
-    float x0[16], x1[16];
-    const uint32_t* col = reinterpret_cast<const uint32_t*>(sV) + tb * 16 * (D / 2) + cp;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t u = col[k * (D / 2)];
-      const T* p = reinterpret_cast<const T*>(&u);
-      x0[k] = to_f32<T>(p[0]);
-      x1[k] = to_f32<T>(p[1]);
-    }
-    uint32_t lo, hi, sc0, sc1;
-    const int c = 2 * cp;
-    phi16(x0, lo, hi, sc0);
-    *reinterpret_cast<uint2*>(sVcode + c * 64 + tb * 8) = make_uint2(lo, hi);
-    phi16(x1, lo, hi, sc1);
-    *reinterpret_cast<uint2*>(sVcode + (c + 1) * 64 + tb * 8) = make_uint2(lo, hi);
-    const int base = (tb >> 2) * 512 + ((c >> 5) & 3) * 4 + (tb & 3);
-    sSF[1][base + (c & 31) * 16] = (uint8_t)sc0;
-    sSF[1][base + ((c + 1) & 31) * 16] = (uint8_t)sc1;
-  }
-  if (qa.nonfinite && !finite) atomicOr(qa.nonfinite, 1u);
-  __syncthreads();
-  for (int i = t; i < D * 4; i += 256) {
-    const int c = i >> 2, q = i & 3;
-    *reinterpret_cast<uint4*>(va.v_data + ((int64_t)bh * D + c) * (Np >> 1) + chunk * 64 + q * 16) =
-        *reinterpret_cast<const uint4*>(sVcode + c * 64 + q * 16);
-  }
-  block_copy16(qa.q_sf + (int64_t)bh * Np * (D / 16) + (int64_t)chunk * 512 * (D / 64), sSF[0], 512 * (D / 64));
-  block_copy16(va.v_sf + (int64_t)bh * 128 * (Np >> 4) + (int64_t)chunk * 1024, sSF[1], 1024);
+  if (lane == 0) km[w] = (float)(total / (double)N);
 }
 
-// ---------------------------------------------------------------------------------- pass B: φ(K - km)
-template <typename T, int D>
-__global__ void __launch_bounds__(256) quant_pass_b_kernel(QKArgs qa) {
-  __shared__ __align__(16) uint8_t sSF[1024];
-  __shared__ __align__(16) float sKm[D];
-  const int chunk = blockIdx.x, bh = blockIdx.y;
-  const int b = bh / qa.H, h = bh % qa.H;
-  const int t = threadIdx.x;
-  for (int i = t; i < 1024 / 16; i += 256) reinterpret_cast<uint4*>(sSF)[i] = make_uint4(0, 0, 0, 0);
-  for (int i = t; i < D; i += 256) sKm[i] = qa.k_mean[(int64_t)bh * D + i];
-  __syncthreads();
-  bool finite = true;
-  const T* kb = reinterpret_cast<const T*>(qa.k) + b * qa.k_sb + h * qa.k_sh;
-  quant_rows<T, D, true>(kb, qa.k_sn, qa.N, chunk * 128, sKm, qa.k_data + ((int64_t)bh * qa.Np + chunk * 128) * (D / 2),
-                         sSF, finite);
-  __syncthreads();
-  block_copy16(qa.k_sf + (int64_t)bh * qa.Np * (D / 16) + (int64_t)chunk * 512 * (D / 64), sSF, 512 * (D / 64));
-}
+// ---------------------------------------------------------------------------------- streaming φ of Q, V, K
+// Persistent kernel over work items (tensor, b·h, 128-token chunk): Q items, then Vᵀ items, then K items
+// (K needs km, written by the K-mean kernels launched before it).  Warp 8 streams the 128 x d input tiles
+// into a kStages-deep smem ring with TMA (4-D tensor maps over the caller's strides; rows >= N arrive as
+// zeros, which quantize to the zero codes/scales the padding needs); warps 0-7 quantize from smem:
+//   Q, K: φ along d, two threads per 16-element block (shuffle for the amax), coalesced 4-byte code stores;
+//   Vᵀ:   φ along tokens through a transposed smem read, codes staged per channel row and stored 64 bytes
+//         per channel; scale bytes of every item go to its SF atoms staged in smem, then 16-byte stores.
+constexpr int kQStages = 3;
 
 template <int D>
-constexpr int qv_smem() {
-  return 128 * D * 2 + D * 64 + 2 * 1024;
+struct QL {
+  static constexpr int kTile = 128 * D * 2;
+  static constexpr int oVcode = kQStages * kTile;  // Vᵀ codes of one item: D channel rows x 64 bytes
+  static constexpr int oSFqk = oVcode + D * 64;     // Q/K SF atoms of one item (512·D/64 bytes)
+  static constexpr int oSFv = oSFqk + 1024;         // Vᵀ SF atoms of one item (1024 bytes, rows >= d stay 0)
+  static constexpr int oBar = oSFv + 1024;
+  static constexpr int kBytes = oBar + 2 * kQStages * 8;
+  static constexpr int kAlloc = kBytes + 128;      // slack for the 128-byte alignment of the TMA tiles
+};
+
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <typename T, int D>
+__global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_constant__ CUtensorMap tm_q,
+                                                              const __grid_constant__ CUtensorMap tm_k,
+                                                              const __grid_constant__ CUtensorMap tm_v, QKArgs qa,
+                                                              VArgs va) {
+  using L = QL<D>;
+  extern __shared__ uint8_t qsm_raw[];
+  __shared__ float s_rcp[128];  // fl32(1/s) per E4M3 scale code (c4); 0 for s = 0
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(qsm_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::oBar);
+  uint64_t* empty = full + kQStages;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int nch = qa.Np >> 7, BH = qa.B * qa.H;
+  const int per_tensor = BH * nch, total = 3 * per_tensor;
+  if (t == 0) {
+    for (int s = 0; s < kQStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);  // one arrival per consumer warp
+    }
+    fence_mbar_init();
+  }
+  for (int i = t; i < 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm + L::oSFv)[i] = make_uint4(0, 0, 0, 0);
+  if (t < 128) {
+    const float sd = e4m3_to_f32((uint32_t)t);
+    s_rcp[t] = (sd == 0.0f || t == 0x7F) ? 0.0f : __frcp_rn(sd);
+  }
+  __syncthreads();
+
+  if (warp == 8) {  // ---------------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      prefetch_tmap(&tm_q);
+      prefetch_tmap(&tm_k);
+      prefetch_tmap(&tm_v);
+      int k = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x, ++k) {
+        const int s = k % kQStages;
+        const int tensor = item / per_tensor, rem = item % per_tensor, bh = rem / nch, chunk = rem % nch;
+        const CUtensorMap* tm = tensor == 0 ? &tm_q : tensor == 1 ? &tm_v : &tm_k;
+        mbar_wait(&empty[s], ((uint32_t)(k / kQStages) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], L::kTile);
+        tma_load_4d(sm + s * L::kTile, tm, &full[s], 0, chunk * 128, bh % qa.H, bh / qa.H);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------------------------ consumers (256)
+  bool finite = true;
+  int k = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x, ++k) {
+    const int s = k % kQStages;
+    const int tensor = item / per_tensor, rem = item % per_tensor, bh = rem / nch, chunk = rem % nch;
+    const T* tile = reinterpret_cast<const T*>(sm + s * L::kTile);
+    mbar_wait(&full[s], (uint32_t)(k / kQStages) & 1u);
+    if (tensor != 1) {  // Q or K: φ along d
+      const bool smooth = tensor == 2;
+      constexpr int kVec = D / 8, kIt = 128 * kVec / 256;
+      const int cv = t % kVec;  // this thread's 8-channel group (fixed: 256 is a multiple of kVec)
+      uint8_t* codes = (smooth ? qa.k_data : qa.q_data) + ((int64_t)bh * qa.Np + chunk * 128) * (D / 2);
+      float km[8];
+      if (smooth) {
+        const float4 m0 = reinterpret_cast<const float4*>(qa.k_mean + (int64_t)bh * D + cv * 8)[0];
+        const float4 m1 = reinterpret_cast<const float4*>(qa.k_mean + (int64_t)bh * D + cv * 8)[1];
+        km[0] = m0.x, km[1] = m0.y, km[2] = m0.z, km[3] = m0.w, km[4] = m1.x, km[5] = m1.y, km[6] = m1.z, km[7] = m1.w;
+      }
+      uint8_t* sfs = sm + L::oSFqk;
+#pragma unroll
+      for (int it = 0; it < kIt; ++it) {
+        const int i = it * 256 + t, r = i / kVec;
+        float x[8];
+        unpack8<T>(reinterpret_cast<const uint4*>(tile)[i], x);
+        if (smooth) {
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const f2 d = fadd2(make_float2(x[e], x[e + 1]), make_float2(-km[e], -km[e + 1]));
+            x[e] = d.x, x[e + 1] = d.y;
+          }
+        }
+        float amax = amax8(x);
+        amax = fmax3_nan(amax, __shfl_xor_sync(0xffffffffu, amax, 1), 0.0f);
+        finite &= isfinite(amax);
+        // padding rows (n >= N) arrive as zeros from TMA; they must stay zero codes / zero scales even
+        // after smoothing (reading c13)
+        const bool real = chunk * 128 + r < qa.N;
+        const uint32_t sc = real ? cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu : 0u;
+        // a zero scale gives all-zero codes (c5; x·0 would keep the sign of x: E2M1 -0 = 0x8)
+        const uint32_t w = sc ? codes8(x, s_rcp[sc]) : 0u;
+        *reinterpret_cast<uint32_t*>(codes + r * (D / 2) + cv * 4) = w;
+        if ((cv & 1) == 0) {
+          const int c = cv >> 1;
+          sfs[(c >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (c & 3)] = (uint8_t)sc;
+        }
+      }
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[s]);  // tile consumed
+      consumer_bar();                             // SF staging complete
+      uint8_t* sf_dst = (smooth ? qa.k_sf : qa.q_sf) + (int64_t)bh * qa.Np * (D / 16) + (int64_t)chunk * 512 * (D / 64);
+      for (int i = t * 16; i < 512 * (D / 64); i += 256 * 16)
+        *reinterpret_cast<uint4*>(sf_dst + i) = *reinterpret_cast<const uint4*>(sfs + i);
+      consumer_bar();  // staging free for the next item
+    } else {  // Vᵀ: φ along tokens
+      uint8_t* vcode = sm + L::oVcode;
+      uint8_t* sfs = sm + L::oSFv;
+      for (int it = t; it < (D / 2) * 8; it += 256) {
+        const int cp = it % (D / 2), tb = it / (D / 2);
+        float x0[16], x1[16];
+        const uint32_t* col = reinterpret_cast<const uint32_t*>(tile) + tb * 16 * (D / 2) + cp;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t u = col[e * (D / 2)];
+          const T* p = reinterpret_cast<const T*>(&u);
+          x0[e] = to_f32<T>(p[0]);
+          x1[e] = to_f32<T>(p[1]);
+        }
+        const int c = 2 * cp;
+        const float a0 = fmax3_nan(amax8(x0), amax8(x0 + 8), 0.0f), a1 = fmax3_nan(amax8(x1), amax8(x1 + 8), 0.0f);
+        finite &= isfinite(a0) & isfinite(a1);
+        const uint32_t sc2 = cvt_e4m3x2(__fmul_rn(a0, kOneSixth), __fmul_rn(a1, kOneSixth));
+        const uint32_t sc0 = sc2 & 0xFFu, sc1 = (sc2 >> 8) & 0xFFu;
+        const float r0 = s_rcp[sc0], r1 = s_rcp[sc1];
+        *reinterpret_cast<uint2*>(vcode + c * 64 + tb * 8) =
+            sc0 ? make_uint2(codes8(x0, r0), codes8(x0 + 8, r0)) : make_uint2(0u, 0u);
+        *reinterpret_cast<uint2*>(vcode + (c + 1) * 64 + tb * 8) =
+            sc1 ? make_uint2(codes8(x1, r1), codes8(x1 + 8, r1)) : make_uint2(0u, 0u);
+        const int base = (tb >> 2) * 512 + ((c >> 5) & 3) * 4 + (tb & 3);
+        sfs[base + (c & 31) * 16] = (uint8_t)sc0;
+        sfs[base + ((c + 1) & 31) * 16] = (uint8_t)sc1;
+      }
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[s]);
+      consumer_bar();
+      for (int i = t; i < D * 4; i += 256) {
+        const int c = i >> 2, q = i & 3;
+        *reinterpret_cast<uint4*>(va.v_data + ((int64_t)bh * D + c) * (qa.Np >> 1) + chunk * 64 + q * 16) =
+            *reinterpret_cast<const uint4*>(vcode + c * 64 + q * 16);
+      }
+      uint8_t* sf_dst = va.v_sf + (int64_t)bh * 128 * (qa.Np >> 4) + (int64_t)chunk * 1024;
+      for (int i = t * 16; i < 1024; i += 256 * 16)
+        *reinterpret_cast<uint4*>(sf_dst + i) = *reinterpret_cast<const uint4*>(sfs + i);
+      consumer_bar();
+    }
+  }
+  if (qa.nonfinite && !finite) atomicOr(qa.nonfinite, 1u);
+}
+
+// 4-D tensor map over a [B][H][N][d] 16-bit operand with element strides (sb, sh, sn): box d x 128 x 1 x 1.
+bool make_input_map(CUtensorMap* m, const void* base, int B, int H, int N, int d, int64_t sb, int64_t sh,
+                    int64_t sn) {
+  auto enc = encode_fn_q();
+  if (!enc) return false;
+  // strides of extent-1 dimensions are irrelevant; give them a valid value
+  if (H == 1) sh = sn * N;
+  if (B == 1) sb = sh * H;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)sn * 2, (cuuint64_t)sh * 2, (cuuint64_t)sb * 2};
+  cuuint32_t box[4] = {(cuuint32_t)d, 128, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <typename T, int D>
 cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t stream) {
+  using L = QL<D>;
   static bool attr_done[64] = {};
+  static int n_sm[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(quant_qv_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         qv_smem<D>());
+    cudaError_t e = cudaFuncSetAttribute(quant_stream_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::kAlloc);
     if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
     attr_done[dev] = true;
   }
+  CUtensorMap tq, tk, tv;
+  if (!make_input_map(&tq, qk.q, qk.B, qk.H, qk.N, D, qk.q_sb, qk.q_sh, qk.q_sn) ||
+      !make_input_map(&tk, qk.k, qk.B, qk.H, qk.N, D, qk.k_sb, qk.k_sh, qk.k_sn) ||
+      !make_input_map(&tv, v.v, qk.B, qk.H, qk.N, D, v.sb, v.sh, v.sn))
+    return cudaErrorInvalidValue;
   const int BH = qk.B * qk.H;
   dim3 grid(qk.Np / 128, BH);
   kmean_kernel<T><<<grid, D / 2, 0, stream>>>(reinterpret_cast<const T*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn, qk.H,
                                               qk.N, D, ws);
-  kmean_final_kernel<<<(BH * D + 127) / 128, 128, 0, stream>>>(ws, qk.Np / 128, qk.N, D, BH * D, qk.k_mean);
-  quant_qv_kernel<T, D><<<grid, 256, qv_smem<D>(), stream>>>(qk, v);
-  quant_pass_b_kernel<T, D><<<grid, 256, 0, stream>>>(qk);
+  kmean_final_kernel<<<(BH * D * 32 + 255) / 256, 256, 0, stream>>>(ws, qk.Np / 128, qk.N, BH * D, qk.k_mean);
+  const int items = 3 * BH * (qk.Np / 128);
+  const int ctas = min(items, 2 * (dev < 64 && n_sm[dev] ? n_sm[dev] : 148));
+  quant_stream_kernel<T, D><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v);
   return cudaGetLastError();
 }
 
