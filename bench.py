@@ -169,6 +169,8 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# our kernels per step: kmean_kernel, kmean_final_kernel, quant_stream_kernel (sage3_quantize_qkv) + attn_fwd_kernel
+LAUNCHES_PER_STEP = 4
 METRIC = "FP4 attention fwd TOPS per B200 (d=128, N=1K-32K) and % of dense FP4 peak"
 
 
@@ -344,7 +346,8 @@ def main():
             "data": "synthetic (seeded Gaussian Q/K/V with outlier channels; synth/)",
             "config": cfg, "pct_fp4_peak": 100 * value / world / fp4_peak,
             "breakdown_ms": {"quantize": q_ms, "attention": a_ms},
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": 5 * n_steps, "launches_per_step": 5,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": LAUNCHES_PER_STEP * n_steps,
+            "launches_per_step": LAUNCHES_PER_STEP,
             "roofline": roofline, "quantize_roofline": quant, "cpu_baseline": cpu, "sweep": sweep,
             "context": {"paper_RTX5090_TOPS": 1038, "paper_B200_theoretical_TOPS": 10000},
         }

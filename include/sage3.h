@@ -108,6 +108,18 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
 sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
                             float softmax_scale, float* lse, void* stream);
 
+/* The same computation restricted to the work units [unit_begin, unit_end) of the flattened (b·h, query
+ * tile) space: unit u covers head bh = u / T and query rows [128·(T-1-u%T), +128) of it, T = N_pad/128
+ * (query tiles of a head are numbered from the last one, the longest under causal masking).  Only those
+ * rows of o (and lse) are written; K/V of every head a unit touches must be quantized in *qkv.  Results
+ * are bitwise identical to the same rows of sage3_attn_fwd (a unit's output does not depend on which other
+ * units share the launch), which is what lets the multi-GPU launcher split heads that do not divide the GPU
+ * count.  Errors: SAGE3_ERR_INVALID_ARG also for unit_begin < 0, unit_end < unit_begin or
+ * unit_end > B·H·T; an empty range enqueues nothing. */
+sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                                  float softmax_scale, float* lse, int64_t unit_begin, int64_t unit_end,
+                                  void* stream);
+
 /* End-to-end convenience path with HOST buffers (for e2e measurements): copies contiguous host
  * q, k, v ([B][H][N][d], in_dtype; pinned memory recommended) to device scratch, quantizes, runs the
  * attention and copies O (contiguous [B][H][N][d], o_dtype) back to o_host — all enqueued on `stream`;

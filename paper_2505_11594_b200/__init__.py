@@ -23,7 +23,7 @@ _DT = {torch.float16: SAGE3_FP16, torch.bfloat16: SAGE3_BF16, torch.float32: SAG
 # Every function include/sage3.h declares (checked by tests/test_abi.py).
 ABI_FUNCTIONS = (
     "sage3_fp4_qkv_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
-    "sage3_attn_fwd", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
+    "sage3_attn_fwd", "sage3_attn_fwd_units", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
     "sage3_last_cuda_error", "sage3_version",
 )
 
@@ -65,6 +65,9 @@ def load() -> ctypes.CDLL:
                                      ctypes.c_void_p, ctypes.c_void_p]
     L.sage3_attn_fwd.argtypes = [ctypes.POINTER(FP4QKVStruct), Tensor4, ctypes.c_int, ctypes.c_int, ctypes.c_float,
                                  ctypes.c_void_p, ctypes.c_void_p]
+    L.sage3_attn_fwd_units.argtypes = [ctypes.POINTER(FP4QKVStruct), Tensor4, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_float, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_void_p]
     L.sage3_forward_host_scratch_bytes.argtypes = [ctypes.c_int] * 6
     L.sage3_forward_host_scratch_bytes.restype = sz
     L.sage3_forward_host.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 6 + [ctypes.c_float, ctypes.c_void_p,
@@ -159,6 +162,21 @@ def sage3_attn_fwd(qkv: FP4QKV, o: torch.Tensor | None = None, *, causal: bool =
     st = load().sage3_attn_fwd(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], 1 if causal else 0,
                                float(softmax_scale), lse_p, _stream(stream))
     _check(st, "sage3_attn_fwd")
+    return o
+
+
+def n_units(qkv: FP4QKV) -> int:
+    """Work units of the (b·h, 128-row query tile) space (see sage3_attn_fwd_units)."""
+    return qkv.B * qkv.H * ((qkv.N + 127) // 128)
+
+
+def sage3_attn_fwd_units(qkv: FP4QKV, o: torch.Tensor, unit_begin: int, unit_end: int, *, causal: bool = False,
+                         softmax_scale: float = 0.0, lse: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sage3_attn_fwd on the work units [unit_begin, unit_end) only (rows of o outside them untouched)."""
+    lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
+    st = load().sage3_attn_fwd_units(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], 1 if causal else 0,
+                                     float(softmax_scale), lse_p, int(unit_begin), int(unit_end), _stream(stream))
+    _check(st, "sage3_attn_fwd_units")
     return o
 
 

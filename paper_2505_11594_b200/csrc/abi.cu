@@ -133,10 +133,14 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
 }
 
-sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
-                            float softmax_scale, float* lse, void* stream) {
+sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                                  float softmax_scale, float* lse, int64_t unit_begin, int64_t unit_end,
+                                  void* stream) {
   if (!qkv || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
   if (qkv->N_pad != npad(qkv->N)) return SAGE3_ERR_INVALID_ARG;
+  const int64_t n_units = (int64_t)qkv->B * qkv->H * (qkv->N_pad / 128);
+  if (unit_begin < 0 || unit_end < unit_begin || unit_end > n_units || unit_end - unit_begin > 0x7FFFFFFF)
+    return SAGE3_ERR_INVALID_ARG;
   if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
   if (!tensor_ok(o, esize_of(o_dtype))) return SAGE3_ERR_INVALID_ARG;
   if (!qkv->q_data || !qkv->k_data || !qkv->v_data || !qkv->q_sf || !qkv->k_sf || !qkv->v_sf)
@@ -155,8 +159,16 @@ sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dty
   a.B = qkv->B, a.H = qkv->H, a.N = qkv->N, a.Np = qkv->N_pad, a.d = qkv->d;
   a.causal = causal ? 1 : 0;
   a.scale = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)qkv->d);
+  a.unit_begin = unit_begin, a.unit_end = unit_end;
   cudaError_t e = sage3::launch_attention(a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
+}
+
+sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                            float softmax_scale, float* lse, void* stream) {
+  if (!qkv || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
+  return sage3_attn_fwd_units(qkv, o, o_dtype, causal, softmax_scale, lse, 0,
+                              (int64_t)qkv->B * qkv->H * (npad(qkv->N) / 128), stream);
 }
 
 // ---------------------------------------------------------------------------------- host e2e path

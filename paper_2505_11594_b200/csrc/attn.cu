@@ -232,9 +232,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Work unit u = unit_begin + blockIdx.x of the flattened (b·h, q-tile) space, q tiles fastest and in
+  // descending order within a head (CTAs of one head run together and share K/V in L2; longest first under
+  // causal masking).  sage3_attn_fwd covers every unit; the multi-GPU launcher gives each rank a range.
   const int n_qt = a.Np >> 7;
-  const int qt = n_qt - 1 - (int)blockIdx.x;  // q tiles fastest (CTAs of one head share K/V in L2),
-  const int bh = blockIdx.y;                  // longest-first under causal masking
+  const int64_t unit = a.unit_begin + (int64_t)blockIdx.x;
+  const int bh = (int)(unit / n_qt);
+  const int qt = n_qt - 1 - (int)(unit % n_qt);
   const int nkv = a.causal ? qt + 1 : n_qt;
 
   if (threadIdx.x == 0) {
@@ -689,8 +693,9 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
       !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
       !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D))
     return cudaErrorInvalidValue;
-  dim3 grid(a.Np / 128, BH);
-  attn_fwd_kernel<D><<<grid, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
+  const int64_t units = a.unit_end - a.unit_begin;
+  if (units <= 0) return cudaSuccess;
+  attn_fwd_kernel<D><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
   return cudaGetLastError();
 }
 

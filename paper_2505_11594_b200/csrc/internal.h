@@ -37,6 +37,7 @@ struct AttnArgs {
   int B, H, N, Np, d;
   int causal;
   float scale;  // softmax scale (S units)
+  int64_t unit_begin, unit_end;  // work units [begin, end) of the flattened (b·h, q-tile) space
 };
 
 // Returns cudaSuccess or the launch / driver error.  `drv_err` receives a CUresult on descriptor failure.

@@ -1,18 +1,26 @@
-"""Multi-GPU launcher for the SageAttention3 forward: one process per GPU (torch.distributed), the flattened
-(b, h) heads split into contiguous balanced shards, no data exchange on the hot path, one final gather.
+"""Multi-GPU launcher for the SageAttention3 forward: one process per GPU (torch.distributed), the work split
+into contiguous cost-balanced ranges of (b·h, 128-row query tile) units, no data exchange on the hot path,
+one final gather.
 
 Why no collective: smoothing K (Alg1 L2), φ and the whole Algorithm 1 loop are per
-(b, h) head — every head is an independent problem — so each rank quantizes and attends its own heads
-and the only communication is collecting O at the end (off the hot path; NCCL gather over NVLink).
+(b, h) head — every head is an independent problem, and within a head every 128-row query tile is an
+independent problem given the head's quantized K and V — so each rank quantizes the heads its units touch,
+runs `sage3_attn_fwd_units` on its units, and the only communication is collecting O at the end (off the
+hot path; NCCL gather over NVLink).  Unit granularity (not whole heads) keeps head counts that do not
+divide the GPU count balanced (C3: 60 heads on 8 GPUs), at the price of a rank re-quantizing the K/V of at
+most two heads it shares with its neighbours (memory-bound work, a few % of a head's attention time).
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
 
+TILE = 128  # query rows per unit (the kernel's B_q)
+
 
 def shard_ranges(n_units: int, world: int) -> list[tuple[int, int]]:
-    """Contiguous, balanced [start, end) split of n_units over world ranks (sizes differ by at most 1)."""
+    """Contiguous, balanced [start, end) split of n_units equal-cost units over world ranks (sizes differ by at
+    most 1)."""
     if world < 1 or n_units < 0:
         raise ValueError("world must be >= 1 and n_units >= 0")
     base, extra = divmod(n_units, world)
@@ -25,50 +33,131 @@ def shard_ranges(n_units: int, world: int) -> list[tuple[int, int]]:
 
 
 def local_heads(B: int, H: int, world: int, rank: int) -> range:
-    """Flattened head ids (b*H + h) owned by `rank`."""
+    """Flattened head ids (b*H + h) of a whole-head split (kept for reference; the launcher splits units)."""
     s, e = shard_ranges(B * H, world)[rank]
     return range(s, e)
 
 
-def _default_compute(q, k, v, causal, softmax_scale):
+def tiles_per_head(N: int) -> int:
+    return (N + TILE - 1) // TILE
+
+
+def unit_cost(u: int, T: int, causal: bool) -> int:
+    """KV tiles a unit processes: unit u is query tile T-1-u%T of its head (the kernel's numbering)."""
+    return T - (u % T) if causal else T
+
+
+def shard_units(B: int, H: int, N: int, causal: bool, world: int) -> list[tuple[int, int]]:
+    """Contiguous [start, end) ranges of the B·H·T unit space whose KV-tile costs are as equal as a contiguous
+    split allows (boundary r is placed where the cost prefix is closest to r/world of the total)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    T = tiles_per_head(N)
+    n = B * H * T
+    if not causal:
+        return shard_ranges(n, world)
+    # prefix cost of whole heads is closed-form; within a head the costs are T, T-1, ..., 1
+    head_cost = T * (T + 1) // 2
+    total = B * H * head_cost
+
+    def prefix(u: int) -> int:  # cost of units [0, u)
+        h, r = divmod(u, T)
+        return h * head_cost + r * T - r * (r - 1) // 2
+
+    bounds = [0]
+    for r in range(1, world):
+        target = total * r / world
+        lo, hi = bounds[-1], n
+        while lo < hi:  # smallest u with prefix(u) >= target
+            mid = (lo + hi) // 2
+            if prefix(mid) < target:
+                lo = mid + 1
+            else:
+                hi = mid
+        u = lo
+        if u > bounds[-1] and abs(prefix(u - 1) - target) < abs(prefix(u) - target):
+            u -= 1
+        bounds.append(max(u, bounds[-1]))
+    bounds.append(n)
+    return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+def unit_rows(u: int, T: int, N: int) -> tuple[int, int, int]:
+    """(flattened head, first row, end row) of unit u."""
+    bh, r = divmod(u, T)
+    qt = T - 1 - r
+    return bh, qt * TILE, min(N, qt * TILE + TILE)
+
+
+def _default_compute(q, k, v, causal, softmax_scale, unit_lo, unit_hi):
     import paper_2505_11594_b200 as s3
 
-    return s3.attention(q, k, v, causal=causal, softmax_scale=softmax_scale)
+    qkv = s3.sage3_quantize_qkv(q, k, v)
+    o = torch.empty_like(q)
+    return s3.sage3_attn_fwd_units(qkv, o, unit_lo, unit_hi, causal=causal, softmax_scale=softmax_scale)
 
 
 def forward_sharded(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
                     softmax_scale: float = 0.0, group=None, gather_to: int = 0, compute=None):
-    """Run the FP4 attention forward on this rank's heads and gather O on rank `gather_to`.
+    """Run the FP4 attention forward on this rank's work units and gather O on rank `gather_to`.
 
-    q, k, v: the full [B, H, N, d] inputs (as every rank sees them; only this rank's heads are read).
-    Returns the full O on `gather_to` and this rank's [n_local, N, d] slice of O elsewhere.
-    `compute(q, k, v, causal, softmax_scale)` maps [1, n_local, N, d] inputs to O; it defaults to the CUDA
-    path (quantize + attention through the C ABI).  Tests substitute a host stub to exercise the sharding
-    and gather logic without a GPU.
+    q, k, v: the full [B, H, N, d] inputs (as every rank sees them; only the heads of this rank's units are
+    read).  Returns the full O on `gather_to`; elsewhere this rank's packed [n_local_units, 128, d] rows.
+    `compute(q, k, v, causal, softmax_scale, unit_lo, unit_hi)` maps the [1, n_heads, N, d] inputs of the
+    touched heads to O for them, valid at least on the rows of units [unit_lo, unit_hi) (numbered within those
+    heads).  It defaults to the CUDA path (sage3_quantize_qkv + sage3_attn_fwd_units through the C ABI);
+    tests substitute a host stub to exercise the sharding and gather logic without a GPU.
     """
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     B, H, N, d = q.shape
-    heads = local_heads(B, H, world, rank)
+    T = tiles_per_head(N)
+    ranges = shard_units(B, H, N, causal, world)
+    u0, u1 = ranges[rank]
     fn = compute or _default_compute
     flat = lambda x: x.reshape(B * H, N, d)
-    sl = slice(heads.start, heads.stop)
-    if len(heads):
-        o_local = fn(flat(q)[sl].unsqueeze(0), flat(k)[sl].unsqueeze(0), flat(v)[sl].unsqueeze(0), causal,
-                     softmax_scale)[0]
-    else:
-        o_local = q.new_empty(0, N, d)
+    packed = q.new_zeros(max(u1 - u0, 0), TILE, d)
+    if u1 > u0:
+        h0, h1 = u0 // T, (u1 - 1) // T + 1
+        sl = slice(h0, h1)
+        o_heads = fn(flat(q)[sl].unsqueeze(0), flat(k)[sl].unsqueeze(0), flat(v)[sl].unsqueeze(0), causal,
+                     softmax_scale, u0 - h0 * T, u1 - h0 * T)[0]
+        idx, valid = _row_index(u0, u1, T, N, h0, q.device)
+        packed.view(-1, d)[valid] = o_heads.reshape(-1, d)[idx[valid]]
     if world == 1:
-        return o_local.reshape(B, H, N, d)
-    # equal-size gather: pad every shard to the largest one
-    ranges = shard_ranges(B * H, world)
+        out = q.new_empty(B * H, N, d)
+        _unpack(out, packed, 0, u1, T, N)
+        return out.reshape(B, H, N, d)
+    # equal-size gather: pad every rank's packed rows to the largest range
     cap = max(e - s for s, e in ranges)
-    buf = o_local.new_zeros(cap, N, d)
-    buf[: o_local.shape[0]] = o_local
+    buf = q.new_zeros(cap, TILE, d)
+    buf[: packed.shape[0]] = packed
     if rank == gather_to:
         parts = [torch.empty_like(buf) for _ in range(world)]
         dist.gather(buf, parts, dst=gather_to, group=group)
-        out = torch.cat([p[: e - s] for p, (s, e) in zip(parts, ranges)])
+        out = q.new_empty(B * H, N, d)
+        for p, (s, e) in zip(parts, ranges):
+            _unpack(out, p, s, e, T, N)
         return out.reshape(B, H, N, d)
     dist.gather(buf, None, dst=gather_to, group=group)
-    return o_local
+    return packed
+
+
+def _row_index(u0: int, u1: int, T: int, N: int, h0: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    """For the packed rows of units [u0, u1) (TILE rows each): the flat row index into a [heads from h0][N]
+    array, and whether the row exists (the last query tile of a head may be ragged)."""
+    u = torch.arange(u0, u1, device=device, dtype=torch.int64)
+    bh, r = u // T, u % T
+    row0 = (T - 1 - r) * TILE
+    rows = row0[:, None] + torch.arange(TILE, device=device, dtype=torch.int64)[None, :]
+    valid = (rows < N).reshape(-1)
+    idx = ((bh - h0)[:, None] * N + rows).reshape(-1)
+    return idx, valid
+
+
+def _unpack(out: torch.Tensor, packed: torch.Tensor, u0: int, u1: int, T: int, N: int):
+    if u1 <= u0:
+        return
+    d = out.shape[-1]
+    idx, valid = _row_index(u0, u1, T, N, 0, out.device)
+    out.view(-1, d)[idx[valid]] = packed[: u1 - u0].reshape(-1, d)[valid]

@@ -158,3 +158,26 @@ def test_forward_host_pipeline_matches_device_path(B, H, N, d, causal):
     stream.synchronize()
     torch.cuda.synchronize()
     assert torch.equal(oh, want.cpu())
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_attn_fwd_units_subranges_bitwise(causal):
+    """sage3_attn_fwd_units on any unit range writes exactly those rows, bitwise equal to the full launch (the
+    invariant the multi-GPU unit split relies on); other rows stay untouched."""
+    B, H, N, d = 1, 3, 1000, 128
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=21, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V)
+    full = s3.sage3_attn_fwd(qkv, causal=causal)
+    T = (N + 127) // 128
+    from paper_2505_11594_b200.multigpu import unit_rows
+    for u0, u1 in [(0, 1), (5, 17), (7, 8), (0, 3 * T)]:
+        o = torch.full_like(full, float("nan"))
+        s3.sage3_attn_fwd_units(qkv, o, u0, u1, causal=causal)
+        torch.cuda.synchronize()
+        written = torch.zeros(B * H, N, dtype=torch.bool)
+        for u in range(u0, u1):
+            bh, r0, r1 = unit_rows(u, T, N)
+            written[bh, r0:r1] = True
+        of, ff = o.reshape(B * H, N, d).cpu(), full.reshape(B * H, N, d).cpu()
+        assert torch.equal(of[written], ff[written])
+        assert torch.isnan(of[~written].float()).all()

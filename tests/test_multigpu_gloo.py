@@ -1,6 +1,7 @@
-"""CPU (gloo, world_size 2) tests of the multi-GPU launcher's host logic: head sharding covers every (b, h)
-exactly once with balanced shards, and the final gather reassembles O in order.  The per-shard compute is a
-host stub here (a per-head function of the inputs); the CUDA path is exercised by the GPU tests and bench."""
+"""CPU (gloo, world_size 2) tests of the multi-GPU launcher's host logic: the (b·h, query-tile) unit split
+covers every unit exactly once with balanced KV-tile cost, and the final gather reassembles O in order.  The
+per-shard compute is a host stub here (a per-head function of the inputs); the CUDA path is exercised by the
+GPU tests and bench."""
 import os
 import socket
 
@@ -9,7 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2505_11594_b200.multigpu import forward_sharded, local_heads, shard_ranges
+from paper_2505_11594_b200.multigpu import (forward_sharded, local_heads, shard_ranges, shard_units, tiles_per_head,
+                                            unit_cost, unit_rows)
 
 
 def test_shard_ranges_cover_and_balance():
@@ -25,8 +27,33 @@ def test_shard_ranges_cover_and_balance():
     assert list(local_heads(2, 30, 8, 7)) == list(range(53, 60))
 
 
-def stub(q, k, v, causal, scale):
-    # a per-head deterministic function standing in for the attention kernel
+@pytest.mark.parametrize("B,H,N,causal,world", [(2, 30, 17776, False, 8), (1, 24, 118800, False, 8),
+                                                 (8, 32, 32768, True, 8), (1, 3, 300, True, 2), (2, 30, 17776, True, 8),
+                                                 (1, 1, 128, True, 4), (1, 5, 1000, True, 3)])
+def test_shard_units_cover_and_balance(B, H, N, causal, world):
+    T = tiles_per_head(N)
+    rs = shard_units(B, H, N, causal, world)
+    assert rs[0][0] == 0 and rs[-1][1] == B * H * T and all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+    costs = [sum(unit_cost(u, T, causal) for u in range(s, e)) for s, e in rs]
+    # a contiguous split is within one unit's cost (<= T KV tiles) of the ideal share
+    assert max(costs) - sum(costs) / world <= T
+    if not causal:
+        assert max(e - s for s, e in rs) - min(e - s for s, e in rs) <= 1
+    # C3 on 8 GPUs: 60 heads x 139 tiles -> 1043/1042 units (vs 8/7 whole heads)
+    if (B, H, N, causal, world) == (2, 30, 17776, False, 8):
+        assert [e - s for s, e in rs] == [1043] * 4 + [1042] * 4
+
+
+def test_unit_rows_numbering():
+    # unit u of a head is query tile T-1-u%T (longest first under causal masking); the last tile is ragged
+    T = tiles_per_head(300)
+    assert T == 3
+    assert unit_rows(0, T, 300) == (0, 256, 300) and unit_rows(2, T, 300) == (0, 0, 128)
+    assert unit_rows(4, T, 300) == (1, 128, 256)
+
+
+def stub(q, k, v, causal, scale, unit_lo=None, unit_hi=None):
+    # a per-head deterministic function standing in for the attention kernel (valid on every row)
     return v * 2.0 + q.sum(-1, keepdim=True) * (0.5 if causal else 1.0)
 
 
@@ -38,14 +65,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B, H, causal, ret):
+def _worker(rank, world, port, B, H, N, causal, ret):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     g = torch.Generator().manual_seed(0)
-    q = torch.randn(B, H, 16, 8, generator=g)
-    k = torch.randn(B, H, 16, 8, generator=g)
-    v = torch.randn(B, H, 16, 8, generator=g)
+    q = torch.randn(B, H, N, 8, generator=g)
+    k = torch.randn(B, H, N, 8, generator=g)
+    v = torch.randn(B, H, N, 8, generator=g)
     out = forward_sharded(q, k, v, causal=causal, compute=stub)
     if rank == 0:
         ret["ok"] = bool(torch.equal(out, stub(q, k, v, causal, 0.0)))
@@ -56,10 +83,11 @@ def _worker(rank, world, port, B, H, causal, ret):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("B,H", [(1, 4), (1, 3), (2, 3)])
-def test_forward_sharded_gather_world2(B, H):
+@pytest.mark.parametrize("B,H,N,causal", [(1, 4, 16, True), (1, 3, 300, True), (2, 3, 200, False), (1, 1, 384, True)])
+def test_forward_sharded_gather_world2(B, H, N, causal):
     mgr = mp.Manager()
     ret = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), B, H, True, ret), nprocs=2, join=True)
-    assert ret["ok"] and ret["shape"] == (B, H, 16, 8)
-    assert ret["local1"][0] == len(local_heads(B, H, 2, 1))
+    mp.spawn(_worker, args=(2, _free_port(), B, H, N, causal, ret), nprocs=2, join=True)
+    assert ret["ok"] and ret["shape"] == (B, H, N, 8)
+    s, e = shard_units(B, H, N, causal, 2)[1]
+    assert ret["local1"][0] == e - s
