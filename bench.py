@@ -258,6 +258,24 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ms_step = elapsed_ms / n_steps
+    # the launcher's one collective, off the hot path: gather every rank's O to rank 0 (NCCL over NVLink),
+    # timed separately (device events, max over ranks)
+    gather = None
+    if dist:
+        parts = [torch.empty_like(O) for _ in range(world)] if rank == 0 else None
+        dist.gather(O, parts, dst=0)  # warm-up
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        dist.gather(O, parts, dst=0)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([g0.elapsed_time(g1)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather = {"ms": t.item(), "bytes_into_rank0": (world - 1) * O.numel() * O.element_size(),
+                  "collective": "torch.distributed.gather (NCCL), after the timed region"}
+        del parts
     ops_rank = attn_ops(B, H, N, d, causal)
     value = ops_rank * world / (ms_step * 1e-3) / 1e12
     q_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_q)
@@ -349,6 +367,7 @@ def main():
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": LAUNCHES_PER_STEP * n_steps,
             "launches_per_step": LAUNCHES_PER_STEP,
             "roofline": roofline, "quantize_roofline": quant, "cpu_baseline": cpu, "sweep": sweep,
+            "final_gather": gather,
             "context": {"paper_RTX5090_TOPS": 1038, "paper_B200_theoretical_TOPS": 10000},
         }
         print(json.dumps(line), flush=True)

@@ -12,6 +12,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline "$@" > /dev/null 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 3 -c 1 -f \
   -o gpurun_out/${TAG}_prof_attn python bench.py --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline "$@" > gpurun_out/${TAG}_ncu_attn.log 2>&1; echo "ncu attn rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"quant|kmean" -s 12 -c 4 -f \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"quant|kmean" -s 9 -c 3 -f \
   -o gpurun_out/${TAG}_prof_quant python bench.py --steps 1 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline "$@" > gpurun_out/${TAG}_ncu_quant.log 2>&1; echo "ncu quant rc=$?"
 ls -la gpurun_out/

@@ -100,7 +100,7 @@ if os.path.exists(lc):
             t[r[iN]].append(float(r[iV].replace(",", "")))
     tot = sum(sum(v) for v in t.values())
     lines = [f"ncu launch list ({tag}; --metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised;"
-             " compare shares, not absolutes). Command: bench.py --steps 2 --warmup 3 (5 steps of 5 launches each"
+             " compare shares, not absolutes). Command: bench.py --steps 2 --warmup 3 (5 steps of 4 launches each"
              " + the synthetic-input generation kernels)",
              f"{'kernel':90s} {'launches':>8s} {'mean_us':>10s} {'share%':>7s}"]
     for name, v in sorted(t.items(), key=lambda x: -sum(x[1])):
