@@ -57,9 +57,9 @@ constexpr int kThreads = 512;
 // Per-thread register budgets after setmaxnreg (one warp of each warpgroup per SM sub-partition:
 // kRegWG0 + 2 kRegSoftmax + kRegCorrection = 512 = 64K registers / 128 lanes).
 #ifndef SAGE3_REG_WG0
-#define SAGE3_REG_WG0 40
-#define SAGE3_REG_SOFTMAX 136
-#define SAGE3_REG_CORRECTION 200
+#define SAGE3_REG_WG0 32
+#define SAGE3_REG_SOFTMAX 144
+#define SAGE3_REG_CORRECTION 192
 #endif
 constexpr uint32_t kRegWG0 = SAGE3_REG_WG0, kRegSoftmax = SAGE3_REG_SOFTMAX, kRegCorrection = SAGE3_REG_CORRECTION;
 static_assert(kRegWG0 + 2 * kRegSoftmax + kRegCorrection <= 512, "register budget");
@@ -411,8 +411,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kv0 = j * 128;
       const int lim = a.causal ? min(a.N - 1, q_row) - kv0 : a.N - 1 - kv0;  // last visible key in tile
       // ---- pass 1: 16-key block maxima of S (reused for the row max and for s_P2).  Masked keys are set
-      //      to -inf and written back to TMEM so pass 2 needs no masking code.  Two 32-column TMEM loads
-      //      are in flight at a time.
+      //      to -inf and written back to TMEM so pass 2 needs no masking code.  All four 32-column TMEM
+      //      loads are in flight together (one round trip; the pass-2 buffers are not live yet).
       float bmax[8];
       auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
@@ -424,19 +424,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
       };
-      {
-        uint32_t va[32], vb[32];
-#pragma unroll
-        for (int c = 0; c < 4; c += 2) {
-          tmem_ld_32x32b_x32(s_addr + 32 * c, va);
-          tmem_ld_32x32b_x32(s_addr + 32 * c + 32, vb);
-          tmem_ld_wait_regs(va);
-          tmem_ld_wait_regs(vb);
-          SAGE3_TRACE_EV(par ? 3 : 0, j, c);
-          pass1(c, va);
-          pass1(c + 1, vb);
-          SAGE3_TRACE_EV(par ? 3 : 0, j, c + 1);
-        }
+      {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
+        uint32_t va[32], vb[32], vc[32], vd[32];
+        tmem_ld_32x32b_x32(s_addr, va);
+        tmem_ld_32x32b_x32(s_addr + 32, vb);
+        tmem_ld_32x32b_x32(s_addr + 64, vc);
+        tmem_ld_32x32b_x32(s_addr + 96, vd);
+        tmem_ld_wait_regs(va);
+        tmem_ld_wait_regs(vb);
+        tmem_ld_wait_regs(vc);
+        tmem_ld_wait_regs(vd);
+        pass1(0, va);
+        pass1(1, vb);
+        pass1(2, vc);
+        pass1(3, vd);
       }
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
