@@ -181,3 +181,31 @@ def test_attn_fwd_units_subranges_bitwise(causal):
         of, ff = o.reshape(B * H, N, d).cpu(), full.reshape(B * H, N, d).cpu()
         assert torch.equal(of[written], ff[written])
         assert torch.isnan(of[~written].float()).all()
+
+
+# The other BASELINE.json configurations at full size, in the bench's launch configuration (one launch over
+# all heads): quantizer bit-exact on sampled heads, attention on sampled rows of those heads vs the oracle.
+# C5 (B=8, H=32, N=32768, causal, 8 GPUs) runs 32 heads of N=32768 per GPU — the C2 causal case above.
+CONFIGS = {
+    "C3-cogvideox": (2, 30, 17776, 64, False, [0, 37, 59]),
+    "C4-hunyuanvideo": (1, 24, 118800, 128, False, [0, 23]),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_paper_config_full_size_sampled(name):
+    from test_gpu_quant import _check_head
+
+    B, H, N, d, causal, heads = CONFIGS[name]
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=5, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V)
+    O = s3.sage3_attn_fwd(qkv, causal=causal, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    Qf, Kf, Vf = (x.reshape(B * H, N, d) for x in (Q, K, V))
+    for bh in heads:
+        _check_head(qkv, bh, Qf[bh].float().cpu().numpy(), Kf[bh].float().cpu().numpy(), Vf[bh].float().cpu().numpy())
+    rows = np.unique(np.concatenate([[0, 1, 127, 128, N - 129, N - 1], np.linspace(0, N - 1, 26).astype(np.int32)]))
+    ref = oracle.attn_fwd(oracle_heads(qkv, heads), causal=causal, scale=1 / math.sqrt(d), rows=rows)
+    Of = O.reshape(B * H, N, d)
+    for i, bh in enumerate(heads):
+        check(Of[bh].float().cpu().numpy()[rows], ref[i], torch.bfloat16, f"{name} head {bh}")
