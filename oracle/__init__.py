@@ -65,6 +65,12 @@ def lib():
             L.oracle_kmean.argtypes = [fp, ctypes.c_int, ctypes.c_int, fp]
             L.oracle_quantize_head.argtypes = [fp, fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                u8p, u8p, u8p, u8p, u8p, u8p, fp]
+            L.oracle_quantize_head_sq.argtypes = [fp, fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                  u8p, u8p, u8p, u8p, u8p, u8p, fp, fp, fp]
+            L.oracle_qmean_tile.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp]
+            L.oracle_attn_fwd_sq.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p,
+                                             fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ip,
+                                             ctypes.c_int, dp, dp]
             L.oracle_dequant.argtypes = [u8p, u8p, ctypes.c_int, ctypes.c_int, dp]
             L.oracle_fp4mm.argtypes = [u8p, u8p, u8p, u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
             L.oracle_two_level_row.restype = ctypes.c_float
@@ -217,34 +223,54 @@ class QuantizedHead:
         self.k_sf = np.zeros((Np, d // 16), np.uint8)
         self.v_sf = np.zeros((d, Np // 16), np.uint8)
         self.km = np.zeros(d, np.float32)
+        self.q_mean = None  # smoothing Q (Alg1 L5): [Np/128][d] fp32 q̄ per 128-row query tile
+        self.ks = None      # smoothing Q: the full-precision smoothed K [Np][d] of Alg1 L8's GEMV
 
 
-def quantize_head(Q, K, V, smooth_k: bool = True) -> QuantizedHead:
-    """Alg1 L2 (smoothing K) + φ of Q, K (along d) and V (along tokens, stored transposed)."""
+def quantize_head(Q, K, V, smooth_k: bool = True, smooth_q: bool = False) -> QuantizedHead:
+    """Alg1 L2 (smoothing K), L5 (smoothing Q, optional) + φ of Q, K (along d) and V (along tokens, stored
+    transposed, P:1184)."""
     Q, K, V = _f32(Q), _f32(K), _f32(V)
     N, d = Q.shape
     h = QuantizedHead(N, d)
-    u8 = ctypes.c_uint8
-    lib().oracle_quantize_head(_p(Q, ctypes.c_float), _p(K, ctypes.c_float), _p(V, ctypes.c_float), N, d,
-                               1 if smooth_k else 0, _p(h.q_codes, u8), _p(h.q_sf, u8), _p(h.k_codes, u8),
-                               _p(h.k_sf, u8), _p(h.v_codes, u8), _p(h.v_sf, u8), _p(h.km, ctypes.c_float))
+    u8, fp = ctypes.c_uint8, ctypes.c_float
+    if smooth_q:
+        h.q_mean = np.zeros((h.Np // 128, d), np.float32)
+        h.ks = np.zeros((h.Np, d), np.float32)
+    lib().oracle_quantize_head_sq(_p(Q, fp), _p(K, fp), _p(V, fp), N, d, 1 if smooth_k else 0,
+                                  1 if smooth_q else 0, _p(h.q_codes, u8), _p(h.q_sf, u8), _p(h.k_codes, u8),
+                                  _p(h.k_sf, u8), _p(h.v_codes, u8), _p(h.v_sf, u8), _p(h.km, fp),
+                                  _p(h.q_mean, fp) if smooth_q else None, _p(h.ks, fp) if smooth_q else None)
     return h
+
+
+def qmean_tile(Q, tile: int) -> np.ndarray:
+    """q̄ of one 128-row query tile (Alg1 L5), in the fixed order of reading c10."""
+    Q = _f32(Q)
+    N, d = Q.shape
+    out = np.zeros(d, np.float32)
+    lib().oracle_qmean_tile(_p(Q, ctypes.c_float), N, d, tile, _p(out, ctypes.c_float))
+    return out
 
 
 def attn_fwd(heads: list[QuantizedHead], *, causal: bool, scale: float, rows=None, bkv: int = 128,
              p_mode: int = PMODE_TWO_LEVEL, want_lse: bool = False):
-    """Alg1 L6-L13 on quantized heads (all same N, d).  Returns O [BH][nrows][d] fp64 (and lse)."""
+    """Alg1 L6-L13 on quantized heads (all same N, d; smoothing Q iff the heads carry q_mean/ks).
+    Returns O [BH][nrows][d] fp64 (and lse)."""
     N, d, Np = heads[0].N, heads[0].d, heads[0].Np
     BH = len(heads)
     rows = np.arange(N, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
     cat = lambda name: np.ascontiguousarray(np.stack([getattr(h, name) for h in heads]))
     qc, qs, kc, ks, vc, vs = (cat(n) for n in ("q_codes", "q_sf", "k_codes", "k_sf", "v_codes", "v_sf"))
+    sq = heads[0].q_mean is not None
+    qm, kf = (cat("q_mean"), cat("ks")) if sq else (None, None)
     O = np.zeros((BH, rows.shape[0], d), np.float64)
     lse = np.zeros((BH, rows.shape[0]), np.float64)
-    u8 = ctypes.c_uint8
-    lib().oracle_attn_fwd(BH, N, d, _p(qc, u8), _p(qs, u8), _p(kc, u8), _p(ks, u8), _p(vc, u8), _p(vs, u8), bkv,
-                          1 if causal else 0, float(scale), p_mode, _p(rows, ctypes.c_int), rows.shape[0],
-                          _p(O, ctypes.c_double), _p(lse, ctypes.c_double))
+    u8, fp = ctypes.c_uint8, ctypes.c_float
+    lib().oracle_attn_fwd_sq(BH, N, d, _p(qc, u8), _p(qs, u8), _p(kc, u8), _p(ks, u8), _p(vc, u8), _p(vs, u8),
+                             _p(qm, fp) if sq else None, _p(kf, fp) if sq else None, bkv, 1 if causal else 0,
+                             float(scale), p_mode, _p(rows, ctypes.c_int), rows.shape[0], _p(O, ctypes.c_double),
+                             _p(lse, ctypes.c_double))
     return (O, lse) if want_lse else O
 
 

@@ -6,12 +6,13 @@
  * links, imports or executes anything under oracle/, and this file shares no code, header, table or
  * constant generator with it.
  *
- * What it computes: Algorithm 1 of the paper WITHOUT smoothing Q (the north_star
- * omits Alg1 L5's q̄ / L8's GEMV), step by step, in the paper's order and notation:
+ * What it computes: Algorithm 1 of the paper, step by step, in the paper's order and
+ * notation; smoothing Q (Alg1 L5's q̄, L8's GEMV) is a switch (off on the north_star path):
  *   Alg1 L2    K = K - mean(K)                                   -> oracle_kmean, oracle_quantize_head
  *   Eq. 1      s = max|X|/6, X̂ = ⌈X/s⌋ over 1x16 blocks -> phi_nvfp4
+ *   Alg1 L5    q̄_i = mean(Q_i), φ(Q_i - q̄_i) (smoothing Q, optional) -> oracle_qmean_tile, oracle_quantize_head_sq
  *   Alg1 L7    φ(K_j^T) along d, φ(V_j) along tokens      -> oracle_quantize_head
- *   Alg1 L8    S = FP4MM(Q̂, s_Q, K̂, s_K)  (Eq. 3)      -> attn_row (exact in fp64)
+ *   Alg1 L8    S = FP4MM(Q̂, s_Q, K̂, s_K) [+ GEMV(q̄_i, K_j^T)]    -> attn_row (exact in fp64)
  *   Alg1 L9    m, P̃ = exp(S - m), l = e^{m_old-m} l + rowsum(P̃)   -> attn_row
  *   Alg1 L10   s_P1 = rowmax(P̃)/(448*6), P̃2 = P̃/s_P1, (s_P2, P̂2) = φ(P̃2)   (§3.2)
  *   Alg1 L11   O = diag(e^{m_old-m}) O + FP4MM(P̂2, s_P2, V̂, s_V) * s_P1
@@ -193,12 +194,40 @@ EXPORT void oracle_kmean(const float* K, int N, int d, float* km) {
  * Inputs are fp32 arrays holding the exact bf16/fp16 input values.
  * smooth_k = 0 disables Alg1 L2 (ablation).
  * ------------------------------------------------------------------------------------------------ */
-EXPORT void oracle_quantize_head(const float* Q, const float* K, const float* V, int N, int d, int smooth_k,
-                                 uint8_t* q_codes, uint8_t* q_sf, uint8_t* k_codes, uint8_t* k_sf,
-                                 uint8_t* v_codes, uint8_t* v_sf, float* km_out) {
+/* ------------------------------------------------------------------------------------------------
+ * Smoothing Q, Alg1 L5 (SageAttention2): q̄_i = mean(Q_i) over the rows of query tile i (B_q = 128
+ * rows, the kernel's query tile) that exist (rows >= N are padding, reading c13).  Same fixed order as the
+ * K mean (reading c10): fp64 sequential sum over the tile's rows in ascending order, divided by the row
+ * count in fp64, rounded once to fp32.
+ * ------------------------------------------------------------------------------------------------ */
+EXPORT void oracle_qmean_tile(const float* Q, int N, int d, int tile, float* qm) {
+  int r0 = tile * 128, r1 = r0 + 128 < N ? r0 + 128 : N;
+  for (int c = 0; c < d; ++c) {
+    double acc = 0.0;
+    for (int n = r0; n < r1; ++n) acc += (double)Q[(size_t)n * d + c];
+    qm[c] = (float)(acc / (double)(r1 - r0));
+  }
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Quantize one head, Alg1 L2 + L5 + L7.  Logical layouts (one 4-bit code per byte):
+ *   q_codes, k_codes [Np][d], q_sf, k_sf [Np][d/16]      (blocks along d, reading c6)
+ *   v_codes [d][Np] (V transposed), v_sf [d][Np/16] (blocks along tokens)
+ * Np = round_up(N, 128); padded tokens get zero codes and zero scales (reading c13).
+ * Inputs are fp32 arrays holding the exact bf16/fp16 input values.
+ * smooth_k = 0 disables Alg1 L2 (ablation).  smooth_q = 1 enables Alg1 L5: Q_i - q̄_i is
+ * quantized (x = fl32(Q - q̄), like K - km) and q̄ [Np/128][d] is returned in q_mean_out; ks_out [Np][d]
+ * (nullable) receives the smoothed K = fl32(K - km) in full precision (zero rows beyond N), the K_j of
+ * Alg1 L8's GEMV.
+ * ------------------------------------------------------------------------------------------------ */
+EXPORT void oracle_quantize_head_sq(const float* Q, const float* K, const float* V, int N, int d, int smooth_k,
+                                    int smooth_q, uint8_t* q_codes, uint8_t* q_sf, uint8_t* k_codes, uint8_t* k_sf,
+                                    uint8_t* v_codes, uint8_t* v_sf, float* km_out, float* q_mean_out,
+                                    float* ks_out) {
   const int Np = (N + 127) / 128 * 128;
   const int C = d / 16;
   float* km = (float*)calloc((size_t)d, sizeof(float));
+  float* qm = (float*)calloc((size_t)d, sizeof(float));
   if (smooth_k) oracle_kmean(K, N, d, km);
   if (km_out) memcpy(km_out, km, sizeof(float) * (size_t)d);
   memset(q_codes, 0, (size_t)Np * d);
@@ -207,12 +236,19 @@ EXPORT void oracle_quantize_head(const float* Q, const float* K, const float* V,
   memset(q_sf, 0, (size_t)Np * C);
   memset(k_sf, 0, (size_t)Np * C);
   memset(v_sf, 0, (size_t)d * (Np / 16));
+  if (q_mean_out) memset(q_mean_out, 0, sizeof(float) * (size_t)(Np / 128) * d);
+  if (ks_out) memset(ks_out, 0, sizeof(float) * (size_t)Np * d);
   float blk[16];
   for (int n = 0; n < N; ++n) {
+    if (n % 128 == 0 && smooth_q) {
+      oracle_qmean_tile(Q, N, d, n / 128, qm);
+      if (q_mean_out) memcpy(&q_mean_out[(size_t)(n / 128) * d], qm, sizeof(float) * (size_t)d);
+    }
     for (int b = 0; b < C; ++b) {
-      for (int i = 0; i < 16; ++i) blk[i] = Q[(size_t)n * d + b * 16 + i];
+      for (int i = 0; i < 16; ++i) blk[i] = Q[(size_t)n * d + b * 16 + i] - qm[b * 16 + i]; /* fl32; qm = 0 if off */
       oracle_phi_nvfp4(blk, &q_codes[(size_t)n * d + b * 16], &q_sf[(size_t)n * C + b]);
       for (int i = 0; i < 16; ++i) blk[i] = K[(size_t)n * d + b * 16 + i] - km[b * 16 + i]; /* fl32 */
+      if (ks_out) memcpy(&ks_out[(size_t)n * d + b * 16], blk, sizeof(float) * 16);
       oracle_phi_nvfp4(blk, &k_codes[(size_t)n * d + b * 16], &k_sf[(size_t)n * C + b]);
     }
   }
@@ -223,6 +259,14 @@ EXPORT void oracle_quantize_head(const float* Q, const float* K, const float* V,
     }
   }
   free(km);
+  free(qm);
+}
+
+EXPORT void oracle_quantize_head(const float* Q, const float* K, const float* V, int N, int d, int smooth_k,
+                                 uint8_t* q_codes, uint8_t* q_sf, uint8_t* k_codes, uint8_t* k_sf,
+                                 uint8_t* v_codes, uint8_t* v_sf, float* km_out) {
+  oracle_quantize_head_sq(Q, K, V, N, d, smooth_k, 0, q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, km_out, NULL,
+                          NULL);
 }
 
 /* Dequantize (Eq. 2): X' = s * X̂, exact in fp64. rows x cols codes, blocks of 16 along cols. */
@@ -289,11 +333,13 @@ EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* co
  * p_mode: TWO_LEVEL (the method), DIRECT (ablation), NONE (no P quantization: the unquantized
  * FlashAttention recurrence, used to pin the tiling against plain softmax attention).
  * Causal (reading c12): key j visible iff j <= qi.  Keys >= N are masked (reading c13).
+ * qbar [d] / Ks [Np][d] (both nullable): smoothing Q — S gets + q̄_i·K_j^T (Alg1 L8).
  * Softmax scale (reading c7): P̃ = exp(scale * (S - m)), S in unscaled units.
  * Returns O[d] = O/l and *lse = scale*m + ln(l).
  * ------------------------------------------------------------------------------------------------ */
 static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int N, int Np, int d, int Bkv,
-                     int causal, int qi, double scale, int p_mode, double* O, double* lse) {
+                     int causal, int qi, double scale, int p_mode, const float* qbar, const float* Ks, double* O,
+                     double* lse) {
   double m = -INFINITY, l = 0.0;
   double* S = (double*)malloc(sizeof(double) * (size_t)Bkv);
   float* Pt = (float*)malloc(sizeof(float) * (size_t)Bkv);
@@ -313,6 +359,11 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
       }
       double acc = 0.0;
       for (int c = 0; c < d; ++c) acc += Qrow[c] * Kd[(size_t)key * d + c];
+      if (qbar) { /* Alg1 L8 smoothing Q: + GEMV(q̄_i, K_j^T) with the full-precision smoothed K (fp64) */
+        double g = 0.0;
+        for (int c = 0; c < d; ++c) g += (double)qbar[c] * (double)Ks[(size_t)key * d + c];
+        acc += g;
+      }
       S[t] = acc;
       if (acc > tmax) tmax = acc;
     }
@@ -361,10 +412,10 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
  * oracle_quantize_head, stacked per head).  rows[nrows] selects the query rows evaluated (rows are
  * independent, so a row sample is exact for those rows).  O: [BH][nrows][d], lse: [BH][nrows] (nullable).
  * OpenMP over (head, row). */
-EXPORT void oracle_attn_fwd(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
-                            const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
-                            const uint8_t* v_sf, int Bkv, int causal, double scale, int p_mode, const int* rows,
-                            int nrows, double* O, double* lse) {
+EXPORT void oracle_attn_fwd_sq(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
+                               const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
+                               const uint8_t* v_sf, const float* q_mean, const float* ks, int Bkv, int causal,
+                               double scale, int p_mode, const int* rows, int nrows, double* O, double* lse) {
   const int Np = (N + 127) / 128 * 128;
   const int C = d / 16;
   for (int h = 0; h < BH; ++h) {
@@ -374,16 +425,27 @@ EXPORT void oracle_attn_fwd(int BH, int N, int d, const uint8_t* q_codes, const 
     oracle_dequant(q_codes + (size_t)h * Np * d, q_sf + (size_t)h * Np * C, Np, d, Qd);
     oracle_dequant(k_codes + (size_t)h * Np * d, k_sf + (size_t)h * Np * C, Np, d, Kd);
     oracle_dequant(v_codes + (size_t)h * Np * d, v_sf + (size_t)h * d * (Np / 16), d, Np, Vt);
+    const float* qm_h = q_mean ? q_mean + (size_t)h * (Np / 128) * d : NULL;
+    const float* ks_h = ks ? ks + (size_t)h * Np * d : NULL;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int r = 0; r < nrows; ++r) {
       int qi = rows[r];
       attn_row(&Qd[(size_t)qi * d], Kd, Vt, N, Np, d, Bkv, causal, qi, scale, p_mode,
-               &O[((size_t)h * nrows + r) * d], lse ? &lse[(size_t)h * nrows + r] : NULL);
+               qm_h ? qm_h + (size_t)(qi / 128) * d : NULL, ks_h, &O[((size_t)h * nrows + r) * d],
+               lse ? &lse[(size_t)h * nrows + r] : NULL);
     }
     free(Qd);
     free(Kd);
     free(Vt);
   }
+}
+
+EXPORT void oracle_attn_fwd(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
+                            const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
+                            const uint8_t* v_sf, int Bkv, int causal, double scale, int p_mode, const int* rows,
+                            int nrows, double* O, double* lse) {
+  oracle_attn_fwd_sq(BH, N, d, q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, NULL, NULL, Bkv, causal, scale, p_mode,
+                     rows, nrows, O, lse);
 }
 
 /* The same tiled recurrence on UNQUANTIZED fp32 inputs (Q [N][d], K [N][d], V [N][d]) with any
@@ -403,7 +465,7 @@ EXPORT void oracle_attn_fwd_float(int N, int d, const float* Q, const float* K, 
   for (int r = 0; r < nrows; ++r) {
     double* Qrow = (double*)malloc(sizeof(double) * (size_t)d);
     for (int c = 0; c < d; ++c) Qrow[c] = Q[(size_t)rows[r] * d + c];
-    attn_row(Qrow, Kd, Vt, N, Np, d, Bkv, causal, rows[r], scale, p_mode, &O[(size_t)r * d],
+    attn_row(Qrow, Kd, Vt, N, Np, d, Bkv, causal, rows[r], scale, p_mode, NULL, NULL, &O[(size_t)r * d],
              lse ? &lse[r] : NULL);
     free(Qrow);
   }
