@@ -64,7 +64,13 @@ typedef struct {
  *   v_sf       : R = 128 rows (channels, rows >= d are zero), C = N_pad/16;  8*N_pad bytes per (b,h)
  *   (the layout tcgen05.cp.32x128b.warpx4 expects; identical to cuBLAS's VEC16_UE4M3 layout)
  * Padding tokens n in [N, N_pad) hold zero codes and zero scales.
- *   k_mean : [B][H][d] fp32, the smoothing-K mean (Alg1 L2). */
+ *   k_mean : [B][H][d] fp32, the smoothing-K mean (Alg1 L2).
+ * Smoothing Q (Alg1 L5 + the GEMV of L8; off on the north_star path): set q_mean and ds non-null.
+ *   q_mean : [B][H][N_pad/128][d] fp32, q̄_i of each 128-row query tile (written by sage3_quantize_qkv,
+ *            which then quantizes Q - q̄_i instead of Q)
+ *   ds     : [B][H][N_pad/128][N_pad] fp32, GEMV(q̄_i, K^T) with the full-precision smoothed K
+ *            (written by sage3_quantize_qkv, added to S = FP4MM(Q̂, K̂) by sage3_attn_fwd)
+ *   Both NULL = no smoothing Q (the north_star path).  Sizes: sage3_smooth_q_sizes(). */
 typedef struct {
   int32_t B, H, N, d, N_pad;
   uint8_t* q_data;
@@ -74,11 +80,16 @@ typedef struct {
   uint8_t* k_sf;
   uint8_t* v_sf;
   float* k_mean;
+  float* q_mean; /* nullable (smoothing Q off) */
+  float* ds;     /* nullable (smoothing Q off) */
 } sage3_fp4_qkv;
 
 /* Host-only size queries (no CUDA calls).  bytes[0..6] = q_data, k_data, v_data, q_sf, k_sf, v_sf,
  * k_mean.  Returns SAGE3_ERR_INVALID_ARG for unsupported shapes. */
 sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]);
+
+/* Host-only size queries for smoothing Q: bytes[0] = q_mean, bytes[1] = ds (see sage3_fp4_qkv). */
+sage3_status sage3_smooth_q_sizes(int B, int H, int N, int d, size_t bytes[2]);
 
 /* Device workspace of sage3_quantize_qkv: fp64 K-mean partial sums, B*H*(N_pad/128)*d*8 bytes. */
 size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d);
@@ -88,8 +99,11 @@ size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d);
  * for an unsupported d. */
 int sage3_kv_tile(int d);
 
-/* Alg1 L2 + L7.  q, k, v: [B][H][N][d] in `in_dtype` (SAGE3_FP16 or SAGE3_BF16).  Fills every array of
- * *out (whose pointers and B,H,N,d fields the caller sets; N_pad is written).  `workspace` must hold
+/* Alg1 L2 + L7 (+ L5 and L8's GEMV when out->q_mean and out->ds are set: q̄_i = fl32(Σ_rows Q / rows) over
+ * the real rows of each 128-row tile in fp64 ascending order, Q̂ = φ(fl32(Q - q̄_i)); ds = q̄_i·fl32(K - km)^T
+ * in fp32; SAGE3_ERR_INVALID_ARG if only one of the two is set).  q, k, v: [B][H][N][d] in `in_dtype`
+ * (SAGE3_FP16 or SAGE3_BF16).  Fills every array of *out (whose pointers and B,H,N,d fields the caller sets;
+ * N_pad is written).  `workspace` must hold
  * sage3_quantize_workspace_bytes().  nonfinite_flag: nullable device u32, OR-set to 1 if any input is
  * NaN/Inf (the codes are then unspecified).
  * Numerics (bit-exact with oracle_quantize_head): km[c] = fl32(Σ_chunks Σ_tokens K / N) in fp64 with the

@@ -22,7 +22,7 @@ _DT = {torch.float16: SAGE3_FP16, torch.bfloat16: SAGE3_BF16, torch.float32: SAG
 
 # Every function include/sage3.h declares (checked by tests/test_abi.py).
 ABI_FUNCTIONS = (
-    "sage3_fp4_qkv_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
+    "sage3_fp4_qkv_sizes", "sage3_smooth_q_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
     "sage3_attn_fwd", "sage3_attn_fwd_units", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
     "sage3_last_cuda_error", "sage3_version",
 )
@@ -40,7 +40,7 @@ class Tensor4(ctypes.Structure):
 class FP4QKVStruct(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("N", ctypes.c_int32), ("d", ctypes.c_int32),
                 ("N_pad", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in (
-                    "q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean")]
+                    "q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean", "q_mean", "ds")]
 
 
 _lib = None
@@ -57,6 +57,7 @@ def load() -> ctypes.CDLL:
     L = ctypes.CDLL(LIB_PATH)
     sz = ctypes.c_size_t
     L.sage3_fp4_qkv_sizes.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(sz)]
+    L.sage3_smooth_q_sizes.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(sz)]
     L.sage3_quantize_workspace_bytes.argtypes = [ctypes.c_int] * 4
     L.sage3_quantize_workspace_bytes.restype = sz
     L.sage3_kv_tile.argtypes = [ctypes.c_int]
@@ -113,6 +114,12 @@ def sage3_fp4_qkv_sizes(B: int, H: int, N: int, d: int) -> list[int]:
     return list(out)
 
 
+def sage3_smooth_q_sizes(B: int, H: int, N: int, d: int) -> list[int]:
+    out = (ctypes.c_size_t * 2)()
+    _check(load().sage3_smooth_q_sizes(B, H, N, d, out), "sage3_smooth_q_sizes")
+    return list(out)
+
+
 def sage3_quantize_workspace_bytes(B: int, H: int, N: int, d: int) -> int:
     return int(load().sage3_quantize_workspace_bytes(B, H, N, d))
 
@@ -122,28 +129,36 @@ class FP4QKV:
 
     NAMES = ("q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean")
 
-    def __init__(self, B: int, H: int, N: int, d: int, device):
+    def __init__(self, B: int, H: int, N: int, d: int, device, smooth_q: bool = False):
         self.B, self.H, self.N, self.d = B, H, N, d
         self.N_pad = (N + 127) // 128 * 128
+        self.smooth_q = smooth_q
         sizes = sage3_fp4_qkv_sizes(B, H, N, d)
         for name, nbytes in zip(self.NAMES, sizes):
             setattr(self, name, torch.empty(nbytes, dtype=torch.uint8, device=device))
+        self.q_mean = self.ds = None
+        if smooth_q:  # Alg1 L5 / L8 GEMV buffers
+            qm_b, ds_b = sage3_smooth_q_sizes(B, H, N, d)
+            self.q_mean = torch.empty(qm_b, dtype=torch.uint8, device=device)
+            self.ds = torch.empty(ds_b, dtype=torch.uint8, device=device)
         self.workspace = torch.empty(max(sage3_quantize_workspace_bytes(B, H, N, d), 16), dtype=torch.uint8,
                                      device=device)
         self.struct = FP4QKVStruct(B, H, N, d, self.N_pad,
-                                   *[getattr(self, n).data_ptr() for n in self.NAMES])
+                                   *[getattr(self, n).data_ptr() for n in self.NAMES],
+                                   self.q_mean.data_ptr() if smooth_q else None,
+                                   self.ds.data_ptr() if smooth_q else None)
 
     def nbytes(self) -> int:
         return sum(getattr(self, n).numel() for n in self.NAMES)
 
 
 def sage3_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: FP4QKV | None = None,
-                       nonfinite: torch.Tensor | None = None, stream=None) -> FP4QKV:
-    """Alg1 L2 + L7 (smoothing K, NVFP4 φ of Q, K, V): see include/sage3.h."""
+                       nonfinite: torch.Tensor | None = None, stream=None, smooth_q: bool = False) -> FP4QKV:
+    """Alg1 L2 + L7 (smoothing K, NVFP4 φ of Q, K, V; + L5 / L8's GEMV with smooth_q): see include/sage3.h."""
     B, H, N, d = q.shape
     assert k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dtype in (torch.float16, torch.bfloat16)
     if out is None:
-        out = FP4QKV(B, H, N, d, q.device)
+        out = FP4QKV(B, H, N, d, q.device, smooth_q=smooth_q)
     flag = ctypes.c_void_p(nonfinite.data_ptr() if nonfinite is not None else None)
     st = load().sage3_quantize_qkv(_t4(q), _t4(k), _t4(v), _DT[q.dtype], B, H, N, d, ctypes.byref(out.struct),
                                    ctypes.c_void_p(out.workspace.data_ptr()), out.workspace.numel(), flag,
@@ -200,9 +215,9 @@ def sage3_forward_host(q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch
 
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
-              softmax_scale: float = 0.0, out_dtype=None, stream=None) -> torch.Tensor:
+              softmax_scale: float = 0.0, out_dtype=None, stream=None, smooth_q: bool = False) -> torch.Tensor:
     """Quantize + attention in one call (the two ABI calls, enqueued on the current stream)."""
-    qkv = sage3_quantize_qkv(q, k, v, stream=stream)
+    qkv = sage3_quantize_qkv(q, k, v, stream=stream, smooth_q=smooth_q)
     return sage3_attn_fwd(qkv, causal=causal, softmax_scale=softmax_scale, out_dtype=out_dtype or q.dtype,
                           stream=stream)
 

@@ -90,6 +90,14 @@ sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]) {
   return SAGE3_OK;
 }
 
+sage3_status sage3_smooth_q_sizes(int B, int H, int N, int d, size_t bytes[2]) {
+  if (!bytes || !shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
+  const size_t BH = (size_t)B * H, Np = (size_t)npad(N), T = Np / 128;
+  bytes[0] = BH * T * d * sizeof(float);   // q_mean
+  bytes[1] = BH * T * Np * sizeof(float);  // ds
+  return SAGE3_OK;
+}
+
 size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d) {
   if (!shape_ok(B, H, N, d)) return 0;
   return (size_t)B * H * (size_t)(npad(N) / 128) * d * sizeof(double);
@@ -109,6 +117,8 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   if (!aligned16(out->q_data) || !aligned16(out->k_data) || !aligned16(out->v_data) || !aligned16(out->q_sf) ||
       !aligned16(out->k_sf) || !aligned16(out->v_sf) || !aligned16(out->k_mean))
     return SAGE3_ERR_INVALID_ARG;
+  if ((out->q_mean == nullptr) != (out->ds == nullptr)) return SAGE3_ERR_INVALID_ARG;
+  if (out->q_mean && (!aligned16(out->q_mean) || !aligned16(out->ds))) return SAGE3_ERR_INVALID_ARG;
   if (!workspace || workspace_bytes < sage3_quantize_workspace_bytes(B, H, N, d)) return SAGE3_ERR_WORKSPACE;
   sage3_status st = device_ok();
   if (st != SAGE3_OK) return st;
@@ -121,6 +131,8 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   qa.B = B, qa.H = H, qa.N = N, qa.Np = out->N_pad, qa.d = d;
   qa.q_data = out->q_data, qa.k_data = out->k_data, qa.q_sf = out->q_sf, qa.k_sf = out->k_sf;
   qa.k_mean = out->k_mean;
+  qa.q_mean = out->q_mean;
+  qa.ds = out->ds;
   qa.nonfinite = nonfinite_flag;
   sage3::VArgs va{};
   va.v = v.ptr;
@@ -149,9 +161,12 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
       !aligned16(qkv->k_sf) || !aligned16(qkv->v_sf))
     return SAGE3_ERR_INVALID_ARG;
   if (!(std::isfinite(softmax_scale))) return SAGE3_ERR_INVALID_ARG;
+  if ((qkv->q_mean == nullptr) != (qkv->ds == nullptr)) return SAGE3_ERR_INVALID_ARG;
+  if (qkv->ds && !aligned16(qkv->ds)) return SAGE3_ERR_INVALID_ARG;
   sage3_status st = device_ok();
   if (st != SAGE3_OK) return st;
   sage3::AttnArgs a{};
+  a.ds = qkv->ds;
   a.q_data = qkv->q_data, a.k_data = qkv->k_data, a.v_data = qkv->v_data;
   a.q_sf = qkv->q_sf, a.k_sf = qkv->k_sf, a.v_sf = qkv->v_sf;
   a.o = o.ptr, a.o_sb = o.stride_b, a.o_sh = o.stride_h, a.o_sn = o.stride_n, a.o_dtype = (int)o_dtype;

@@ -14,6 +14,8 @@ struct QKArgs {
   int B, H, N, Np, d;
   uint8_t *q_data, *k_data, *q_sf, *k_sf;
   float* k_mean;  // written by the K-mean pass, read by quant_qk
+  float* q_mean;  // smoothing Q (nullable): [B][H][Np/128][d]
+  float* ds;      // smoothing Q (nullable): [B][H][Np/128][Np] GEMV(q̄_i, K^T)
   uint32_t* nonfinite;
 };
 
@@ -37,6 +39,7 @@ struct AttnArgs {
   int B, H, N, Np, d;
   int causal;
   float scale;  // softmax scale (S units)
+  const float* ds;  // smoothing Q (nullable): [B][H][Np/128][Np], added to S
   int64_t unit_begin, unit_end;  // work units [begin, end) of the flattened (b·h, q-tile) space
 };
 

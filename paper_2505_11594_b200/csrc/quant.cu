@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
   using L = QL<D>;
   extern __shared__ uint8_t qsm_raw[];
   __shared__ float s_rcp[128];  // fl32(1/s) per E4M3 scale code (c4); 0 for s = 0
+  __shared__ __align__(16) float s_qm[D];  // smoothing Q: q̄ of the current Q tile
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(qsm_raw) + 127) & ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::oBar);
   uint64_t* empty = full + kQStages;
@@ -222,13 +223,28 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
     mbar_wait(&full[s], (uint32_t)(k / kQStages) & 1u);
     if (tensor != 1) {  // Q or K: φ along d
       const bool smooth = tensor == 2;
+      const bool sub = smooth || qa.q_mean != nullptr;  // x = fl32(X - mean): K - km, or Q - q̄ (Alg1 L5)
       constexpr int kVec = D / 8, kIt = 128 * kVec / 256;
       const int cv = t % kVec;  // this thread's 8-channel group (fixed: 256 is a multiple of kVec)
       uint8_t* codes = (smooth ? qa.k_data : qa.q_data) + ((int64_t)bh * qa.Np + chunk * 128) * (D / 2);
+      if (!smooth && sub) {
+        // smoothing Q: q̄ of this 128-row tile, fp64 sequential over its real rows in ascending order,
+        // divided by the row count, rounded once (the order of reading c10)
+        if (t < D) {
+          const int nr = min(128, qa.N - chunk * 128);
+          double acc = 0.0;
+          for (int r = 0; r < nr; ++r) acc += (double)to_f32<T>(tile[r * D + t]);
+          const float qm = (float)(acc / (double)nr);
+          s_qm[t] = qm;
+          qa.q_mean[((int64_t)bh * nch + chunk) * D + t] = qm;
+        }
+        consumer_bar();
+      }
       float km[8];
-      if (smooth) {
-        const float4 m0 = reinterpret_cast<const float4*>(qa.k_mean + (int64_t)bh * D + cv * 8)[0];
-        const float4 m1 = reinterpret_cast<const float4*>(qa.k_mean + (int64_t)bh * D + cv * 8)[1];
+      if (sub) {
+        const float* msrc = smooth ? qa.k_mean + (int64_t)bh * D + cv * 8 : s_qm + cv * 8;
+        const float4 m0 = reinterpret_cast<const float4*>(msrc)[0];
+        const float4 m1 = reinterpret_cast<const float4*>(msrc)[1];
         km[0] = m0.x, km[1] = m0.y, km[2] = m0.z, km[3] = m0.w, km[4] = m1.x, km[5] = m1.y, km[6] = m1.z, km[7] = m1.w;
       }
       uint8_t* sfs = sm + L::oSFqk;
@@ -237,7 +253,7 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
         const int i = it * 256 + t, r = i / kVec;
         float x[8];
         unpack8<T>(reinterpret_cast<const uint4*>(tile)[i], x);
-        if (smooth) {
+        if (sub) {
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
             const f2 d = fadd2(make_float2(x[e], x[e + 1]), make_float2(-km[e], -km[e + 1]));
@@ -311,6 +327,58 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
   if (qa.nonfinite && !finite) atomicOr(qa.nonfinite, 1u);
 }
 
+// ---------------------------------------------------------------------------------- smoothing Q: ds
+// ds[bh][i][key] = Σ_c q̄_i[c]·Ks[key][c], Ks = fl32(K - km) (Alg1 L8's GEMV(q̄_i, K_j^T) with the
+// full-precision smoothed K), fp32 FFMA2 on the CUDA cores.  grid (Np/128 key chunks, B·H), 256 threads;
+// thread (ig, kg) owns 8 query tiles x 4 keys of each 64-tile block.  Keys >= N get Ks = 0 (they are masked).
+template <typename T, int D>
+__global__ void __launch_bounds__(256) smooth_q_ds_kernel(QKArgs qa) {
+  extern __shared__ __align__(16) float dsm_f[];
+  float* kst = dsm_f;            // [D][128] smoothed K of this key chunk, transposed
+  float* qmt = dsm_f + D * 128;  // [D][64] q̄ of 64 query tiles, transposed
+  const int chunk = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / qa.H, h = bh % qa.H;
+  const int t = threadIdx.x, nt = qa.Np >> 7;
+  const T* kb = reinterpret_cast<const T*>(qa.k) + b * qa.k_sb + h * qa.k_sh;
+  for (int i = t; i < 128 * D; i += 256) {
+    const int key = i / D, c = i % D, n = chunk * 128 + key;
+    const float kv = n < qa.N ? __fsub_rn(to_f32<T>(kb[(int64_t)n * qa.k_sn + c]), qa.k_mean[(int64_t)bh * D + c]) : 0.0f;
+    kst[c * 128 + key] = kv;
+  }
+  const int kg = t & 31, ig = t >> 5;
+  for (int i0 = 0; i0 < nt; i0 += 64) {
+    __syncthreads();  // kst written / previous block's qmt consumed
+    for (int i = t; i < 64 * D; i += 256) {
+      const int ti = i / D, c = i % D;
+      qmt[c * 64 + ti] = i0 + ti < nt ? qa.q_mean[((int64_t)bh * nt + i0 + ti) * D + c] : 0.0f;
+    }
+    __syncthreads();
+    f2 acc[8][2];
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) acc[ii][0] = acc[ii][1] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int c = 0; c < D; ++c) {
+      const float4 a0 = reinterpret_cast<const float4*>(qmt + c * 64 + ig * 8)[0];
+      const float4 a1 = reinterpret_cast<const float4*>(qmt + c * 64 + ig * 8)[1];
+      const float4 bb = reinterpret_cast<const float4*>(kst + c * 128)[kg];
+      const f2 b01 = make_float2(bb.x, bb.y), b23 = make_float2(bb.z, bb.w);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) {
+        acc[ii][0] = ffma2(make_float2(av[ii], av[ii]), b01, acc[ii][0]);
+        acc[ii][1] = ffma2(make_float2(av[ii], av[ii]), b23, acc[ii][1]);
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) {
+      const int ti = i0 + ig * 8 + ii;
+      if (ti < nt)
+        *reinterpret_cast<float4*>(qa.ds + ((int64_t)bh * nt + ti) * qa.Np + chunk * 128 + kg * 4) =
+            make_float4(acc[ii][0].x, acc[ii][0].y, acc[ii][1].x, acc[ii][1].y);
+    }
+  }
+}
+
 // 4-D tensor map over a [B][H][N][d] 16-bit operand with element strides (sb, sh, sn): box d x 128 x 1 x 1.
 bool make_input_map(CUtensorMap* m, const void* base, int B, int H, int N, int d, int64_t sb, int64_t sh,
                     int64_t sn) {
@@ -355,6 +423,16 @@ cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t 
   const int items = 3 * BH * (qk.Np / 128);
   const int ctas = min(items, 2 * (dev < 64 && n_sm[dev] ? n_sm[dev] : 148));
   quant_stream_kernel<T, D><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v);
+  if (qk.q_mean) {  // smoothing Q: the GEMV term, after every q̄ of the head is written
+    static bool ds_attr[64] = {};
+    constexpr int kDsSmem = (D * 128 + D * 64) * 4;
+    if (dev < 64 && !ds_attr[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(smooth_q_ds_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDsSmem);
+      if (e != cudaSuccess) return e;
+      ds_attr[dev] = true;
+    }
+    smooth_q_ds_kernel<T, D><<<grid, 256, kDsSmem, stream>>>(qk);
+  }
   return cudaGetLastError();
 }
 

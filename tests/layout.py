@@ -31,11 +31,16 @@ def decode_head(qkv, bh: int):
     ks = qkv.k_sf.view(-1, Np * d // 16)[bh].cpu().numpy()
     vs = qkv.v_sf.view(-1, 128 * Np // 16)[bh].cpu().numpy()
     km = qkv.k_mean.view(torch_float32()).view(-1, d)[bh].cpu().numpy()
-    return {
+    out = {
         "q_codes": unpack_codes(qd, Np, d), "k_codes": unpack_codes(kd, Np, d), "v_codes": unpack_codes(vd, d, Np),
         "q_sf": sf_atoms_to_logical(qs, Np, d // 16), "k_sf": sf_atoms_to_logical(ks, Np, d // 16),
         "v_sf_full": sf_atoms_to_logical(vs, 128, Np // 16), "km": km,
     }
+    if getattr(qkv, "smooth_q", False):  # smoothing Q: q̄ per tile and the GEMV term
+        T = Np // 128
+        out["q_mean"] = qkv.q_mean.view(torch_float32()).view(-1, T, d)[bh].cpu().numpy()
+        out["ds"] = qkv.ds.view(torch_float32()).view(-1, T, Np)[bh].cpu().numpy()
+    return out
 
 
 def torch_float32():

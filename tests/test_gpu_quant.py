@@ -93,3 +93,26 @@ def test_hardware_converts_match_oracle_codecs():
     got = decode_head(qkv, 0)["q_codes"][:N]
     want = oracle.e2m1_encode_array(Xb.float().numpy().reshape(-1) * np.float32(1.0)).reshape(N, d)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("N", [1, 129, 300, 1000])
+def test_quantize_smooth_q_bit_exact(d, N):
+    """Smoothing Q (Alg1 L5): q̄ per 128-row tile and the codes/scales of Q - q̄ bit-exact with the oracle; the
+    GEMV term ds = q̄_i·K_s^T (fp32 on the GPU) within fp32 accumulation error of the oracle's fp64 value."""
+    B, H = 1, 2
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=3 * N + d, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V, smooth_q=True)
+    torch.cuda.synchronize()
+    for bh in range(B * H):
+        q, k, v = (x[0, bh].float().cpu().numpy() for x in (Q, K, V))
+        want = oracle.quantize_head(q, k, v, smooth_q=True)
+        got = decode_head(qkv, bh)
+        np.testing.assert_array_equal(got["km"], want.km)
+        np.testing.assert_array_equal(got["q_mean"], want.q_mean)
+        for name in ("q_codes", "q_sf", "k_codes", "k_sf", "v_codes"):
+            np.testing.assert_array_equal(got[name], getattr(want, name), err_msg=name)
+        ref = want.q_mean.astype(np.float64) @ want.ks.astype(np.float64).T  # [T][Np]
+        bound = np.abs(want.q_mean).astype(np.float64) @ np.abs(want.ks).astype(np.float64).T
+        err = np.abs(got["ds"][:, :N] - ref[:, :N])
+        assert np.all(err <= 1e-6 * bound[:, :N] + 1e-30), err.max()
