@@ -170,12 +170,15 @@ def run_reference(args):
 
 
 # our kernels per step: kmean_kernel, kmean_final_kernel, quant_stream_kernel (sage3_quantize_qkv) + attn_fwd_kernel
+# (+ smooth_q_ds_kernel with --smooth-q)
 LAUNCHES_PER_STEP = 4
 METRIC = "FP4 attention fwd TOPS per B200 (d=128, N=1K-32K) and % of dense FP4 peak"
 
 
 def workload_config(args, d):
     name = f"B=1,H={args.heads},N={args.n},d={d},{'causal' if args.causal else 'non-causal'}"
+    if getattr(args, "smooth_q", False):
+        name += ",smooth-q"
     return {"workload": name, "B": 1, "H": args.heads, "N": args.n, "d": d, "causal": bool(args.causal),
             "per_rank": True, "parallelism": f"heads-sharded x{args.gpus}",
             "l2": "inputs larger than L2 (3 x %.0f MB bf16 vs 126 MB)" % (args.heads * args.n * d * 2 / 1e6)}
@@ -193,6 +196,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--smooth-q", action="store_true", help="Alg1 with smoothing Q (NEXT #1; off on the north_star path)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -218,7 +222,7 @@ def main():
     for i in range(H):
         Q[0, i], K[0, i], V[0, i] = synth.make_head(N, d, seed=0, b=0, h=rank * H + i, H=H * world,
                                                     dtype=torch.bfloat16, device=dev)
-    qkv = s3.FP4QKV(B, H, N, d, dev)
+    qkv = s3.FP4QKV(B, H, N, d, dev, smooth_q=args.smooth_q)
     O = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -364,8 +368,8 @@ def main():
             "data": "synthetic (seeded Gaussian Q/K/V with outlier channels; synth/)",
             "config": cfg, "pct_fp4_peak": 100 * value / world / fp4_peak,
             "breakdown_ms": {"quantize": q_ms, "attention": a_ms},
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": LAUNCHES_PER_STEP * n_steps,
-            "launches_per_step": LAUNCHES_PER_STEP,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": (LAUNCHES_PER_STEP + args.smooth_q) * n_steps,
+            "launches_per_step": LAUNCHES_PER_STEP + args.smooth_q,
             "roofline": roofline, "quantize_roofline": quant, "cpu_baseline": cpu, "sweep": sweep,
             "final_gather": gather,
             "context": {"paper_RTX5090_TOPS": 1038, "paper_B200_theoretical_TOPS": 10000},

@@ -45,6 +45,7 @@ using namespace ptx;
 constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
+constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
 #ifndef SAGE3_POLY_MASK
 #define SAGE3_POLY_MASK 0x1111
 #endif
@@ -93,8 +94,9 @@ struct Layout {
   static constexpr int oVSF = oKSF + kKStages * kQKSF;
   static constexpr int oPSF = oVSF + kVStages * kVSF;
   static constexpr int oXchg = oPSF + kPBufs * kPSF;            // float [kXSlots][2][128]: tmax_j, rowsum(P̃2_j)
-  static constexpr int oBar = oXchg + kXSlots * 2 * 128 * 4;
-  static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + kXSlots;
+  static constexpr int oDs = oXchg + kXSlots * 2 * 128 * 4;  // smoothing Q: ds rows of 128 keys, kDsStages slots
+  static constexpr int oBar = oDs + kDsStages * 512;
+  static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + kXSlots + 2 * kDsStages;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
@@ -205,7 +207,7 @@ __device__ unsigned long long g_trace[2][8][128][8];
   } while (0)
 #endif
 
-template <int D>
+template <int D, bool kSQ>  // kSQ: smoothing Q (S += ds, Alg1 L8's GEMV term)
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const AttnArgs a) {
@@ -229,6 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = b_empty + kSBufs;    // softmax -> MMA: P̂2_j / s_P2 in smem buffer j%4, S_j consumed
   uint64_t* p_empty = p_full + kPBufs;    // MMA -> softmax: PV_j done with smem buffer j%4
   uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8
+  uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (TMA)
+  uint64_t* ds_empty = ds_full + kDsStages;  // softmax -> V producer: slot read
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -261,6 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_empty[b], 1);
     }
     for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 4);
+    for (int s = 0; s < kDsStages; ++s) {
+      mbar_init(&ds_full[s], 1);
+      mbar_init(&ds_empty[s], 4);  // one arrival per softmax warp of the tile's warpgroup
+    }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -306,6 +314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------------------------ TMA producer: V
       if (elect_one()) {
         for (int j = 0; j < nkv; ++j) {
+          if constexpr (kSQ) {  // ds[bh][qt][128 j .. 128 j + 128): the GEMV term of this (query, key) tile
+            const int ds_st = j % kDsStages;
+            mbar_wait(&ds_empty[ds_st], ((uint32_t)(j / kDsStages) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&ds_full[ds_st], 512);
+            bulk_load(smem + L::oDs + ds_st * 512, a.ds + ((int64_t)bh * n_qt + qt) * a.Np + j * 128, 512,
+                      &ds_full[ds_st]);
+          }
           const int st = j % kVStages;
           mbar_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
@@ -416,15 +431,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       float bmax[8];
       auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
+        if constexpr (kSQ) {  // Alg1 L8: S += GEMV(q̄_i, K_j^T), the same 128-vector for every row (broadcast)
+          const uint32_t ds_s = smem_u32(smem + L::oDs + (j % kDsStages) * 512) + c * 128;
+#pragma unroll
+          for (int t = 0; t < 32; t += 4) {
+            float4 g;
+            lds_f4(ds_s + t * 4, g);
+            const f2 lo = fadd2(make_float2(f[t], f[t + 1]), make_float2(g.x, g.y));
+            const f2 hi = fadd2(make_float2(f[t + 2], f[t + 3]), make_float2(g.z, g.w));
+            f[t] = lo.x, f[t + 1] = lo.y, f[t + 2] = hi.x, f[t + 3] = hi.y;
+          }
+        }
         if constexpr (masked) {
 #pragma unroll
           for (int t = 0; t < 32; ++t) f[t] = (32 * c + t > lim) ? -INFINITY : f[t];
-          tmem_st_32x32b_x32(s_addr + 32 * c, v);
         }
+        if constexpr (masked || kSQ) tmem_st_32x32b_x32(s_addr + 32 * c, v);  // pass 2 reads the final S
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
       };
-      {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
+      if constexpr (kSQ) mbar_wait(&ds_full[j % kDsStages], (uint32_t)(j / kDsStages) & 1u);
+      if constexpr (kSQ) {  // two loads in flight (the ds chunk needs registers too)
+        uint32_t va[32], vb[32];
+#pragma unroll
+        for (int c = 0; c < 4; c += 2) {
+          tmem_ld_32x32b_x32(s_addr + 32 * c, va);
+          tmem_ld_32x32b_x32(s_addr + 32 * c + 32, vb);
+          tmem_ld_wait_regs(va);
+          tmem_ld_wait_regs(vb);
+          pass1(c, va);
+          pass1(c + 1, vb);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_empty[j % kDsStages]);  // ds slot read by this warp
+      } else {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
         uint32_t va[32], vb[32], vc[32], vd[32];
         tmem_ld_32x32b_x32(s_addr, va);
         tmem_ld_32x32b_x32(s_addr + 32, vb);
@@ -442,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
       const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb)
-      if constexpr (masked) tmem_st_wait();
+      if constexpr (masked || kSQ) tmem_st_wait();
       uint32_t va[32], vb[32];
       tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
       // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
@@ -677,14 +717,14 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D>
+template <int D, bool kSQ>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
   using L = Layout<D>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
@@ -696,14 +736,15 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_fwd_kernel<D><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
+  attn_fwd_kernel<D, kSQ><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream) {
-  return a.d == 128 ? launch_d<128>(a, stream) : launch_d<64>(a, stream);
+  if (a.ds) return a.d == 128 ? launch_d<128, true>(a, stream) : launch_d<64, true>(a, stream);
+  return a.d == 128 ? launch_d<128, false>(a, stream) : launch_d<64, false>(a, stream);
 }
 
 #ifdef SAGE3_TRACE

@@ -209,3 +209,35 @@ def test_paper_config_full_size_sampled(name):
     Of = O.reshape(B * H, N, d)
     for i, bh in enumerate(heads):
         check(Of[bh].float().cpu().numpy()[rows], ref[i], torch.bfloat16, f"{name} head {bh}")
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("N,d", [(300, 64), (1000, 128), (128, 128)])
+def test_attention_smooth_q_parity(N, d, causal):
+    """Smoothing Q (Alg1 L5 + L8's GEMV, NEXT #1): the GPU path (q̄ tiles, Q - q̄ codes, ds = q̄·K_s^T in fp32,
+    S += ds in pass 1) against the oracle's fp64 Algorithm 1 with smoothing Q, north_star tolerance."""
+    B, H = 1, 2
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=11 * N + d, dtype=torch.bfloat16, device="cuda")
+    Q = Q + 4.0 * torch.randn(1, H, 1, d, device="cuda", dtype=torch.float32).to(torch.bfloat16)  # shared offset
+    qkv = s3.sage3_quantize_qkv(Q, K, V, smooth_q=True)
+    O = s3.sage3_attn_fwd(qkv, causal=causal, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    heads = [oracle.quantize_head(*(x[0, bh].float().cpu().numpy() for x in (Q, K, V)), smooth_q=True)
+             for bh in range(B * H)]
+    ref = oracle.attn_fwd(heads, causal=causal, scale=1 / math.sqrt(d))
+    for bh in range(B * H):
+        check(O[0, bh].cpu().numpy(), ref[bh], torch.float32, f"head {bh}")
+
+
+def test_smooth_q_improves_accuracy_on_gpu():
+    """The paper's reason for smoothing Q, measured on the GPU path: queries sharing a large offset."""
+    N, d = 2048, 128
+    Q, K, V = synth.make_qkv(1, 1, N, d, seed=12, dtype=torch.bfloat16, device="cuda")
+    Q = (Q.float() + 6.0 * torch.randn(1, 1, 1, d, device="cuda")).to(torch.bfloat16)
+    rows = np.arange(0, N, 16, dtype=np.int32)
+    ref = oracle.reference_attention(Q[0, 0].float().cpu().numpy(), K[0, 0].float().cpu().numpy(),
+                                     V[0, 0].float().cpu().numpy(), causal=False, scale=1 / math.sqrt(d), rows=rows)
+    m0 = oracle.accuracy_metrics(ref, s3.attention(Q, K, V)[0, 0].float().cpu().numpy()[rows])
+    m1 = oracle.accuracy_metrics(ref, s3.attention(Q, K, V, smooth_q=True)[0, 0].float().cpu().numpy()[rows])
+    print("GPU without / with smoothing Q:", m0, m1)
+    assert m1["cos_sim"] > m0["cos_sim"]
