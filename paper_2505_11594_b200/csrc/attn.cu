@@ -119,7 +119,13 @@ __device__ __forceinline__ f2 ex2_poly2(f2 x) {
   const f2 t = fadd2(x, make_float2(kMagic, kMagic));
   const f2 jf = fadd2(t, make_float2(-kMagic, -kMagic));  // rint(x), exact
   const f2 f = fadd2(x, make_float2(-jf.x, -jf.y));       // x - rint(x), exact (Sterbenz)
-#if SAGE3_POLY_DEGREE == 4
+#if SAGE3_POLY_DEGREE == 3
+  // degree 3 (max rel. error 7.5e-5)
+  f2 p = make_float2(0.055171605199575424f, 0.055171605199575424f);
+  p = ffma2(p, f, make_float2(0.2426111400127411f, 0.2426111400127411f));
+  p = ffma2(p, f, make_float2(0.6932610273361206f, 0.6932610273361206f));
+  p = ffma2(p, f, make_float2(0.9999280571937561f, 0.9999280571937561f));
+#elif SAGE3_POLY_DEGREE == 4
   // degree 4 (max rel. error 2.7e-6: below the E2M1 decision noise, reading c14)
   f2 p = make_float2(0.009570094756782055f, 0.009570094756782055f);
   p = ffma2(p, f, make_float2(0.05591786280274391f, 0.05591786280274391f));
