@@ -45,6 +45,10 @@ using namespace ptx;
 constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
+#ifndef SAGE3_X_ARRIVALS
+#define SAGE3_X_ARRIVALS 128
+#endif
+constexpr int kXArrivals = SAGE3_X_ARRIVALS;  // x_full arrivals per tile: 128 (per thread) or 4 (per warp)
 constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
 #ifndef SAGE3_POLY_MASK
 #define SAGE3_POLY_MASK 0x1111
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[b], 4);  // one arrival per softmax warp
       mbar_init(&p_empty[b], 1);
     }
-    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 4);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], kXArrivals);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
       mbar_init(&ds_empty[s], 4);  // one arrival per softmax warp of the tile's warpgroup
@@ -580,10 +584,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       sts_f32(xchg_s + slot * 1024 + 512, rowsum);
       tc_fence_before();
       fence_proxy_async_smem();
+      // (tmax, rowsum) -> correction: every thread releases its own slot writes on x_full, so the hand-off is
+      // ordered per thread (compute-sanitizer racecheck clean); P̂2 -> MMA: one arrival per warp after the
+      // warp's proxy fences
+      if constexpr (kXArrivals == 128) mbar_arrive(&x_full[slot]);
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&p_full[pb]);
-        mbar_arrive(&x_full[slot]);
+        if constexpr (kXArrivals == 4) mbar_arrive(&x_full[slot]);
       }
       SAGE3_TRACE_WARP(1 + par, j, 4);
     };
