@@ -51,7 +51,10 @@ int esize_of(sage3_dtype t) { return t == SAGE3_FP32 ? 4 : 2; }
 
 // sage3_forward_host pipeline: head groups and the library-owned streams (one set per device, created on
 // first use, never destroyed: they live as long as the process, like the kernels' attribute setup).
-constexpr int kHostGroups = 8;
+#ifndef SAGE3_HOST_GROUPS
+#define SAGE3_HOST_GROUPS 32
+#endif
+constexpr int kHostGroups = SAGE3_HOST_GROUPS;
 struct Pipe {
   cudaStream_t s[3];
 };
