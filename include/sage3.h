@@ -136,9 +136,12 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
 
 /* End-to-end convenience path with HOST buffers (for e2e measurements): copies contiguous host
  * q, k, v ([B][H][N][d], in_dtype; pinned memory recommended) to device scratch, quantizes, runs the
- * attention and copies O (contiguous [B][H][N][d], o_dtype) back to o_host — all enqueued on `stream`;
- * the caller synchronizes the stream before reading o_host.  `scratch` (device) must hold
- * sage3_forward_host_scratch_bytes(). */
+ * attention and copies O (contiguous [B][H][N][d], o_dtype) back to o_host.  The work is split into up to
+ * 32 groups of consecutive heads and pipelined over three library-owned streams of the current device
+ * (copy-in of group g+1 and copy-out of group g-1 overlap the compute of group g); events order it after
+ * the caller's prior work on `stream` and make `stream` wait for the last copy-out, so the call behaves as
+ * if everything were enqueued on `stream`: the caller synchronizes `stream` before reading o_host.
+ * `scratch` (device) must hold sage3_forward_host_scratch_bytes().  No smoothing Q on this path. */
 size_t sage3_forward_host_scratch_bytes(int B, int H, int N, int d, sage3_dtype in_dtype, sage3_dtype o_dtype);
 sage3_status sage3_forward_host(const void* q_host, const void* k_host, const void* v_host, sage3_dtype in_dtype,
                                 int B, int H, int N, int d, int causal, float softmax_scale, void* o_host,
