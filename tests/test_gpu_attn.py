@@ -241,3 +241,39 @@ def test_smooth_q_improves_accuracy_on_gpu():
     m1 = oracle.accuracy_metrics(ref, s3.attention(Q, K, V, smooth_q=True)[0, 0].float().cpu().numpy()[rows])
     print("GPU without / with smoothing Q:", m0, m1)
     assert m1["cos_sim"] > m0["cos_sim"]
+
+
+@pytest.mark.parametrize("o_dtype", [torch.bfloat16, torch.float32])
+def test_strided_output_and_lse(o_dtype):
+    """O written through arbitrary (16-byte aligned) strides: a [B, H, N, d] view into a wider, head-major
+    buffer; the rows and columns outside the view stay untouched; LSE matches the contiguous launch."""
+    B, H, N, d = 2, 2, 300, 64
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=8, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V)
+    want = s3.sage3_attn_fwd(qkv, causal=True, out_dtype=o_dtype)
+    big = torch.full((H, B, N + 8, 2 * d), 7.0, dtype=o_dtype, device="cuda")
+    view = big[:, :, 4:4 + N, d:].permute(1, 0, 2, 3)  # [B, H, N, d], strides (2d(N+8), B·2d(N+8), 2d, 1)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device="cuda")
+    lse_c = torch.empty_like(lse)
+    s3.sage3_attn_fwd(qkv, view, causal=True, lse=lse)
+    s3.sage3_attn_fwd(qkv, want, causal=True, lse=lse_c)
+    torch.cuda.synchronize()
+    assert torch.equal(view, want)
+    assert torch.equal(lse, lse_c)
+    mask = torch.ones_like(big, dtype=torch.bool)
+    mask[:, :, 4:4 + N, d:] = False
+    assert (big[mask] == 7.0).all()
+
+
+def test_abi_rejects_bad_unit_ranges_and_half_smooth_q():
+    Q, K, V = synth.make_qkv(1, 1, 256, 64, seed=2, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V)
+    o = torch.empty_like(Q)
+    n = s3.n_units(qkv)
+    for lo, hi in [(-1, 1), (2, 1), (0, n + 1)]:
+        with pytest.raises(s3.Sage3Error):
+            s3.sage3_attn_fwd_units(qkv, o, lo, hi)
+    s3.sage3_attn_fwd_units(qkv, o, 1, 1)  # empty range: nothing enqueued, OK
+    qkv.struct.q_mean = qkv.k_mean.data_ptr()  # q_mean without ds
+    with pytest.raises(s3.Sage3Error):
+        s3.sage3_attn_fwd(qkv, o)
