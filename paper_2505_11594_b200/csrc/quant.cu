@@ -340,16 +340,27 @@ __global__ void __launch_bounds__(256) smooth_q_ds_kernel(QKArgs qa) {
   const int b = bh / qa.H, h = bh % qa.H;
   const int t = threadIdx.x, nt = qa.Np >> 7;
   const T* kb = reinterpret_cast<const T*>(qa.k) + b * qa.k_sb + h * qa.k_sh;
-  for (int i = t; i < 128 * D; i += 256) {
-    const int key = i / D, c = i % D, n = chunk * 128 + key;
-    const float kv = n < qa.N ? __fsub_rn(to_f32<T>(kb[(int64_t)n * qa.k_sn + c]), qa.k_mean[(int64_t)bh * D + c]) : 0.0f;
-    kst[c * 128 + key] = kv;
+  // keys fastest across threads: each thread reads 8 channels of one key (16 bytes) and writes them down
+  // the transposed tile, consecutive threads hitting consecutive banks
+  for (int i = t; i < 128 * (D / 8); i += 256) {
+    const int key = i % 128, c8 = i / 128, n = chunk * 128 + key;
+    float x[8];
+    if (n < qa.N) {
+      unpack8<T>(*reinterpret_cast<const uint4*>(kb + (int64_t)n * qa.k_sn + c8 * 8), x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = __fsub_rn(x[e], qa.k_mean[(int64_t)bh * D + c8 * 8 + e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = 0.0f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) kst[(c8 * 8 + e) * 128 + key] = x[e];
   }
   const int kg = t & 31, ig = t >> 5;
   for (int i0 = 0; i0 < nt; i0 += 64) {
     __syncthreads();  // kst written / previous block's qmt consumed
-    for (int i = t; i < 64 * D; i += 256) {
-      const int ti = i / D, c = i % D;
+    for (int i = t; i < 64 * D; i += 256) {  // tiles fastest across threads (conflict-free transposed store)
+      const int ti = i % 64, c = i / 64;
       qmt[c * 64 + ti] = i0 + ti < nt ? qa.q_mean[((int64_t)bh * nt + i0 + ti) * D + c] : 0.0f;
     }
     __syncthreads();
