@@ -67,6 +67,12 @@ def lib():
                                                u8p, u8p, u8p, u8p, u8p, u8p, fp]
             L.oracle_quantize_head_sq.argtypes = [fp, fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                   u8p, u8p, u8p, u8p, u8p, u8p, fp, fp, fp]
+            L.oracle_quantize_head_fmt.argtypes = [fp, fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                   ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p, fp, fp, fp]
+            L.oracle_attn_fwd_fmt.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p,
+                                              fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                              ctypes.c_int, ip, ctypes.c_int, dp, dp]
+            L.oracle_dequant_fmt.argtypes = [u8p, u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
             L.oracle_qmean_tile.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp]
             L.oracle_attn_fwd_sq.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p,
                                              fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ip,
@@ -166,6 +172,15 @@ def e4m3_table() -> np.ndarray:
     return np.array([e4m3_decode(c) for c in range(256)])
 
 
+def dequant_fmt(codes: np.ndarray, sf: np.ndarray, fmt: int) -> np.ndarray:
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    sf = np.ascontiguousarray(sf, dtype=np.uint8)
+    out = np.zeros(codes.shape, np.float64)
+    lib().oracle_dequant_fmt(_p(codes, ctypes.c_uint8), _p(sf, ctypes.c_uint8), codes.shape[0], codes.shape[1], fmt,
+                             _p(out, ctypes.c_double))
+    return out
+
+
 def dequant(codes: np.ndarray, sf: np.ndarray) -> np.ndarray:
     """φ^-1 (Eq. 2) for codes [R][C] with scales [R][C/16]; exact fp64."""
     codes = np.ascontiguousarray(codes, dtype=np.uint8)
@@ -210,35 +225,39 @@ def kmean(K) -> np.ndarray:
     return km
 
 
-class QuantizedHead:
-    """Logical-layout NVFP4 codes of one head (one code per byte): q/k [Np][d], v [d][Np]."""
+FMT_NVFP4, FMT_MXFP4 = 0, 1  # E4M3 scales per 16 (the method) / E8M0 scales per 32 (Tab1a ablation)
 
-    def __init__(self, N, d):
+
+class QuantizedHead:
+    """Logical-layout FP4 codes of one head (one code per byte): q/k [Np][d], v [d][Np]; fmt NVFP4 or MXFP4."""
+
+    def __init__(self, N, d, fmt: int = FMT_NVFP4):
         Np = (N + 127) // 128 * 128
-        self.N, self.d, self.Np = N, d, Np
+        G = 32 if fmt == FMT_MXFP4 else 16
+        self.N, self.d, self.Np, self.fmt = N, d, Np, fmt
         self.q_codes = np.zeros((Np, d), np.uint8)
         self.k_codes = np.zeros((Np, d), np.uint8)
         self.v_codes = np.zeros((d, Np), np.uint8)
-        self.q_sf = np.zeros((Np, d // 16), np.uint8)
-        self.k_sf = np.zeros((Np, d // 16), np.uint8)
-        self.v_sf = np.zeros((d, Np // 16), np.uint8)
+        self.q_sf = np.zeros((Np, d // G), np.uint8)
+        self.k_sf = np.zeros((Np, d // G), np.uint8)
+        self.v_sf = np.zeros((d, Np // G), np.uint8)
         self.km = np.zeros(d, np.float32)
         self.q_mean = None  # smoothing Q (Alg1 L5): [Np/128][d] fp32 q̄ per 128-row query tile
         self.ks = None      # smoothing Q: the full-precision smoothed K [Np][d] of Alg1 L8's GEMV
 
 
-def quantize_head(Q, K, V, smooth_k: bool = True, smooth_q: bool = False) -> QuantizedHead:
+def quantize_head(Q, K, V, smooth_k: bool = True, smooth_q: bool = False, fmt: int = FMT_NVFP4) -> QuantizedHead:
     """Alg1 L2 (smoothing K), L5 (smoothing Q, optional) + φ of Q, K (along d) and V (along tokens, stored
-    transposed, P:1184)."""
+    transposed); fmt = FMT_MXFP4 for the Tab1a data-type ablation."""
     Q, K, V = _f32(Q), _f32(K), _f32(V)
     N, d = Q.shape
-    h = QuantizedHead(N, d)
+    h = QuantizedHead(N, d, fmt)
     u8, fp = ctypes.c_uint8, ctypes.c_float
     if smooth_q:
         h.q_mean = np.zeros((h.Np // 128, d), np.float32)
         h.ks = np.zeros((h.Np, d), np.float32)
-    lib().oracle_quantize_head_sq(_p(Q, fp), _p(K, fp), _p(V, fp), N, d, 1 if smooth_k else 0,
-                                  1 if smooth_q else 0, _p(h.q_codes, u8), _p(h.q_sf, u8), _p(h.k_codes, u8),
+    lib().oracle_quantize_head_fmt(_p(Q, fp), _p(K, fp), _p(V, fp), N, d, 1 if smooth_k else 0,
+                                  1 if smooth_q else 0, fmt, _p(h.q_codes, u8), _p(h.q_sf, u8), _p(h.k_codes, u8),
                                   _p(h.k_sf, u8), _p(h.v_codes, u8), _p(h.v_sf, u8), _p(h.km, fp),
                                   _p(h.q_mean, fp) if smooth_q else None, _p(h.ks, fp) if smooth_q else None)
     return h
@@ -267,8 +286,9 @@ def attn_fwd(heads: list[QuantizedHead], *, causal: bool, scale: float, rows=Non
     O = np.zeros((BH, rows.shape[0], d), np.float64)
     lse = np.zeros((BH, rows.shape[0]), np.float64)
     u8, fp = ctypes.c_uint8, ctypes.c_float
-    lib().oracle_attn_fwd_sq(BH, N, d, _p(qc, u8), _p(qs, u8), _p(kc, u8), _p(ks, u8), _p(vc, u8), _p(vs, u8),
-                             _p(qm, fp) if sq else None, _p(kf, fp) if sq else None, bkv, 1 if causal else 0,
+    lib().oracle_attn_fwd_fmt(BH, N, d, _p(qc, u8), _p(qs, u8), _p(kc, u8), _p(ks, u8), _p(vc, u8), _p(vs, u8),
+                             _p(qm, fp) if sq else None, _p(kf, fp) if sq else None, heads[0].fmt, bkv,
+                             1 if causal else 0,
                              float(scale), p_mode, _p(rows, ctypes.c_int), rows.shape[0], _p(O, ctypes.c_double),
                              _p(lse, ctypes.c_double))
     return (O, lse) if want_lse else O

@@ -11,6 +11,7 @@
  *   Alg1 L2    K = K - mean(K)                                   -> oracle_kmean, oracle_quantize_head
  *   Eq. 1      s = max|X|/6, X̂ = ⌈X/s⌋ over 1x16 blocks -> phi_nvfp4
  *   Alg1 L5    q̄_i = mean(Q_i), φ(Q_i - q̄_i) (smoothing Q, optional) -> oracle_qmean_tile, oracle_quantize_head_sq
+ *   Tab1a      MXFP4 instead of NVFP4 for every φ (ablation, fmt = 1)    -> oracle_quantize_head_fmt, oracle_attn_fwd_fmt
  *   Alg1 L7    φ(K_j^T) along d, φ(V_j) along tokens      -> oracle_quantize_head
  *   Alg1 L8    S = FP4MM(Q̂, s_Q, K̂, s_K) [+ GEMV(q̄_i, K_j^T)]    -> attn_row (exact in fp64)
  *   Alg1 L9    m, P̃ = exp(S - m), l = e^{m_old-m} l + rowsum(P̃)   -> attn_row
@@ -215,17 +216,20 @@ EXPORT void oracle_qmean_tile(const float* Q, int N, int d, int tile, float* qm)
  *   v_codes [d][Np] (V transposed), v_sf [d][Np/16] (blocks along tokens)
  * Np = round_up(N, 128); padded tokens get zero codes and zero scales (reading c13).
  * Inputs are fp32 arrays holding the exact bf16/fp16 input values.
- * smooth_k = 0 disables Alg1 L2 (ablation).  smooth_q = 1 enables Alg1 L5: Q_i - q̄_i is
+ * smooth_k = 0 disables Alg1 L2 (ablation).  fmt = 1 is the MXFP4 ablation (Tab1a: 1x32
+ * blocks with E8M0 scales rounded up, oracle_phi_mxfp4; scale arrays then have d/32 resp. Np/32 columns).
+ * smooth_q = 1 enables Alg1 L5: Q_i - q̄_i is
  * quantized (x = fl32(Q - q̄), like K - km) and q̄ [Np/128][d] is returned in q_mean_out; ks_out [Np][d]
  * (nullable) receives the smoothed K = fl32(K - km) in full precision (zero rows beyond N), the K_j of
  * Alg1 L8's GEMV.
  * ------------------------------------------------------------------------------------------------ */
-EXPORT void oracle_quantize_head_sq(const float* Q, const float* K, const float* V, int N, int d, int smooth_k,
-                                    int smooth_q, uint8_t* q_codes, uint8_t* q_sf, uint8_t* k_codes, uint8_t* k_sf,
-                                    uint8_t* v_codes, uint8_t* v_sf, float* km_out, float* q_mean_out,
-                                    float* ks_out) {
+EXPORT void oracle_quantize_head_fmt(const float* Q, const float* K, const float* V, int N, int d, int smooth_k,
+                                     int smooth_q, int fmt, uint8_t* q_codes, uint8_t* q_sf, uint8_t* k_codes,
+                                     uint8_t* k_sf, uint8_t* v_codes, uint8_t* v_sf, float* km_out,
+                                     float* q_mean_out, float* ks_out) {
   const int Np = (N + 127) / 128 * 128;
-  const int C = d / 16;
+  const int G = fmt ? 32 : 16; /* block size: NVFP4 1x16 (E4M3 scales), MXFP4 1x32 (E8M0 scales) */
+  const int C = d / G;
   float* km = (float*)calloc((size_t)d, sizeof(float));
   float* qm = (float*)calloc((size_t)d, sizeof(float));
   if (smooth_k) oracle_kmean(K, N, d, km);
@@ -235,31 +239,42 @@ EXPORT void oracle_quantize_head_sq(const float* Q, const float* K, const float*
   memset(v_codes, 0, (size_t)Np * d);
   memset(q_sf, 0, (size_t)Np * C);
   memset(k_sf, 0, (size_t)Np * C);
-  memset(v_sf, 0, (size_t)d * (Np / 16));
+  memset(v_sf, 0, (size_t)d * (Np / G));
   if (q_mean_out) memset(q_mean_out, 0, sizeof(float) * (size_t)(Np / 128) * d);
   if (ks_out) memset(ks_out, 0, sizeof(float) * (size_t)Np * d);
-  float blk[16];
+  float blk[32];
   for (int n = 0; n < N; ++n) {
     if (n % 128 == 0 && smooth_q) {
       oracle_qmean_tile(Q, N, d, n / 128, qm);
       if (q_mean_out) memcpy(&q_mean_out[(size_t)(n / 128) * d], qm, sizeof(float) * (size_t)d);
     }
     for (int b = 0; b < C; ++b) {
-      for (int i = 0; i < 16; ++i) blk[i] = Q[(size_t)n * d + b * 16 + i] - qm[b * 16 + i]; /* fl32; qm = 0 if off */
-      oracle_phi_nvfp4(blk, &q_codes[(size_t)n * d + b * 16], &q_sf[(size_t)n * C + b]);
-      for (int i = 0; i < 16; ++i) blk[i] = K[(size_t)n * d + b * 16 + i] - km[b * 16 + i]; /* fl32 */
-      if (ks_out) memcpy(&ks_out[(size_t)n * d + b * 16], blk, sizeof(float) * 16);
-      oracle_phi_nvfp4(blk, &k_codes[(size_t)n * d + b * 16], &k_sf[(size_t)n * C + b]);
+      for (int i = 0; i < G; ++i) blk[i] = Q[(size_t)n * d + b * G + i] - qm[b * G + i]; /* fl32; qm = 0 if off */
+      if (fmt) oracle_phi_mxfp4(blk, &q_codes[(size_t)n * d + b * G], &q_sf[(size_t)n * C + b]);
+      else oracle_phi_nvfp4(blk, &q_codes[(size_t)n * d + b * G], &q_sf[(size_t)n * C + b]);
+      for (int i = 0; i < G; ++i) blk[i] = K[(size_t)n * d + b * G + i] - km[b * G + i]; /* fl32 */
+      if (ks_out) memcpy(&ks_out[(size_t)n * d + b * G], blk, sizeof(float) * (size_t)G);
+      if (fmt) oracle_phi_mxfp4(blk, &k_codes[(size_t)n * d + b * G], &k_sf[(size_t)n * C + b]);
+      else oracle_phi_nvfp4(blk, &k_codes[(size_t)n * d + b * G], &k_sf[(size_t)n * C + b]);
     }
   }
   for (int c = 0; c < d; ++c) {
-    for (int t0 = 0; t0 < Np; t0 += 16) {
-      for (int i = 0; i < 16; ++i) blk[i] = (t0 + i < N) ? V[(size_t)(t0 + i) * d + c] : 0.0f;
-      oracle_phi_nvfp4(blk, &v_codes[(size_t)c * Np + t0], &v_sf[(size_t)c * (Np / 16) + t0 / 16]);
+    for (int t0 = 0; t0 < Np; t0 += G) {
+      for (int i = 0; i < G; ++i) blk[i] = (t0 + i < N) ? V[(size_t)(t0 + i) * d + c] : 0.0f;
+      if (fmt) oracle_phi_mxfp4(blk, &v_codes[(size_t)c * Np + t0], &v_sf[(size_t)c * (Np / G) + t0 / G]);
+      else oracle_phi_nvfp4(blk, &v_codes[(size_t)c * Np + t0], &v_sf[(size_t)c * (Np / G) + t0 / G]);
     }
   }
   free(km);
   free(qm);
+}
+
+EXPORT void oracle_quantize_head_sq(const float* Q, const float* K, const float* V, int N, int d, int smooth_k,
+                                    int smooth_q, uint8_t* q_codes, uint8_t* q_sf, uint8_t* k_codes, uint8_t* k_sf,
+                                    uint8_t* v_codes, uint8_t* v_sf, float* km_out, float* q_mean_out,
+                                    float* ks_out) {
+  oracle_quantize_head_fmt(Q, K, V, N, d, smooth_k, smooth_q, 0, q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, km_out,
+                           q_mean_out, ks_out);
 }
 
 EXPORT void oracle_quantize_head(const float* Q, const float* K, const float* V, int N, int d, int smooth_k,
@@ -269,12 +284,19 @@ EXPORT void oracle_quantize_head(const float* Q, const float* K, const float* V,
                           NULL);
 }
 
-/* Dequantize (Eq. 2): X' = s * X̂, exact in fp64. rows x cols codes, blocks of 16 along cols. */
-EXPORT void oracle_dequant(const uint8_t* codes, const uint8_t* sf, int rows, int cols, double* out) {
+/* Dequantize (Eq. 2): X' = s * X̂, exact in fp64. rows x cols codes, blocks of 16 along cols (E4M3
+ * scales) or, fmt = 1, blocks of 32 with E8M0 scales (2^(code - 127)). */
+EXPORT void oracle_dequant_fmt(const uint8_t* codes, const uint8_t* sf, int rows, int cols, int fmt, double* out) {
+  const int G = fmt ? 32 : 16;
   for (int r = 0; r < rows; ++r)
-    for (int c = 0; c < cols; ++c)
-      out[(size_t)r * cols + c] =
-          oracle_e2m1_decode(codes[(size_t)r * cols + c]) * oracle_e4m3_decode(sf[(size_t)r * (cols / 16) + c / 16]);
+    for (int c = 0; c < cols; ++c) {
+      const uint8_t sc = sf[(size_t)r * (cols / G) + c / G];
+      const double s = fmt ? ldexp(1.0, (int)sc - 127) : oracle_e4m3_decode(sc);
+      out[(size_t)r * cols + c] = oracle_e2m1_decode(codes[(size_t)r * cols + c]) * s;
+    }
+}
+EXPORT void oracle_dequant(const uint8_t* codes, const uint8_t* sf, int rows, int cols, double* out) {
+  oracle_dequant_fmt(codes, sf, rows, cols, 0, out);
 }
 
 /* FP4MM, Eq. 3: C = φ^-1(A) φ^-1(B)^T, triple loop in fp64 (exact for NVFP4 operands
@@ -304,10 +326,14 @@ EXPORT void oracle_fp4mm(const uint8_t* a_codes, const uint8_t* a_sf, const uint
 #define PMODE_DIRECT 1
 #define PMODE_NONE 2
 
-EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* codes, uint8_t* sf) {
-  float p2[16];
+EXPORT float oracle_two_level_row_fmt(const float* P, int n, int p_mode, int fmt, uint8_t* codes, uint8_t* sf) {
+  const int G = fmt ? 32 : 16;
+  float p2[32];
   if (p_mode == PMODE_DIRECT) {
-    for (int b = 0; b < n; b += 16) oracle_phi_nvfp4(&P[b], &codes[b], &sf[b / 16]);
+    for (int b = 0; b < n; b += G) {
+      if (fmt) oracle_phi_mxfp4(&P[b], &codes[b], &sf[b / G]);
+      else oracle_phi_nvfp4(&P[b], &codes[b], &sf[b / G]);
+    }
     return 1.0f;
   }
   float pmax = 0.0f;
@@ -316,14 +342,18 @@ EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* co
   float sP1 = pmax / 2688.0f; /* 448 * 6 */
   if (sP1 == 0.0f) {
     memset(codes, 0, (size_t)n);
-    memset(sf, 0, (size_t)n / 16);
+    memset(sf, 0, (size_t)n / G);
     return 0.0f;
   }
-  for (int b = 0; b < n; b += 16) {
-    for (int i = 0; i < 16; ++i) p2[i] = P[b + i] / sP1;
-    oracle_phi_nvfp4(p2, &codes[b], &sf[b / 16]);
+  for (int b = 0; b < n; b += G) {
+    for (int i = 0; i < G; ++i) p2[i] = P[b + i] / sP1;
+    if (fmt) oracle_phi_mxfp4(p2, &codes[b], &sf[b / G]);
+    else oracle_phi_nvfp4(p2, &codes[b], &sf[b / G]);
   }
   return sP1;
+}
+EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* codes, uint8_t* sf) {
+  return oracle_two_level_row_fmt(P, n, p_mode, 0, codes, sf);
 }
 
 /* ------------------------------------------------------------------------------------------------
@@ -338,8 +368,8 @@ EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* co
  * Returns O[d] = O/l and *lse = scale*m + ln(l).
  * ------------------------------------------------------------------------------------------------ */
 static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int N, int Np, int d, int Bkv,
-                     int causal, int qi, double scale, int p_mode, const float* qbar, const float* Ks, double* O,
-                     double* lse) {
+                     int causal, int qi, double scale, int p_mode, const float* qbar, const float* Ks, int fmt,
+                     double* O, double* lse) {
   double m = -INFINITY, l = 0.0;
   double* S = (double*)malloc(sizeof(double) * (size_t)Bkv);
   float* Pt = (float*)malloc(sizeof(float) * (size_t)Bkv);
@@ -383,8 +413,9 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
     if (p_mode == PMODE_NONE) {
       sP1 = 1.0;
     } else {
-      sP1 = (double)oracle_two_level_row(Pt, Bkv, p_mode, pc, ps);
-      for (int t = 0; t < Bkv; ++t) Pq[t] = oracle_e2m1_decode(pc[t]) * oracle_e4m3_decode(ps[t / 16]);
+      sP1 = (double)oracle_two_level_row_fmt(Pt, Bkv, p_mode, fmt, pc, ps);
+      for (int t = 0; t < Bkv; ++t)
+        Pq[t] = oracle_e2m1_decode(pc[t]) * (fmt ? ldexp(1.0, (int)ps[t / 32] - 127) : oracle_e4m3_decode(ps[t / 16]));
     }
     /* Alg1 L11: O = diag(alpha) O + FP4MM(P̂2, s_P2, V̂, s_V) * s_P1 (inner sum exact in fp64) */
     for (int c = 0; c < d; ++c) {
@@ -412,32 +443,41 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
  * oracle_quantize_head, stacked per head).  rows[nrows] selects the query rows evaluated (rows are
  * independent, so a row sample is exact for those rows).  O: [BH][nrows][d], lse: [BH][nrows] (nullable).
  * OpenMP over (head, row). */
-EXPORT void oracle_attn_fwd_sq(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
-                               const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
-                               const uint8_t* v_sf, const float* q_mean, const float* ks, int Bkv, int causal,
-                               double scale, int p_mode, const int* rows, int nrows, double* O, double* lse) {
+EXPORT void oracle_attn_fwd_fmt(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
+                                const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
+                                const uint8_t* v_sf, const float* q_mean, const float* ks, int fmt, int Bkv, int causal,
+                                double scale, int p_mode, const int* rows, int nrows, double* O, double* lse) {
   const int Np = (N + 127) / 128 * 128;
-  const int C = d / 16;
+  const int G = fmt ? 32 : 16;
+  const int C = d / G;
   for (int h = 0; h < BH; ++h) {
     double* Qd = (double*)malloc(sizeof(double) * (size_t)Np * d);
     double* Kd = (double*)malloc(sizeof(double) * (size_t)Np * d);
     double* Vt = (double*)malloc(sizeof(double) * (size_t)Np * d);
-    oracle_dequant(q_codes + (size_t)h * Np * d, q_sf + (size_t)h * Np * C, Np, d, Qd);
-    oracle_dequant(k_codes + (size_t)h * Np * d, k_sf + (size_t)h * Np * C, Np, d, Kd);
-    oracle_dequant(v_codes + (size_t)h * Np * d, v_sf + (size_t)h * d * (Np / 16), d, Np, Vt);
+    oracle_dequant_fmt(q_codes + (size_t)h * Np * d, q_sf + (size_t)h * Np * C, Np, d, fmt, Qd);
+    oracle_dequant_fmt(k_codes + (size_t)h * Np * d, k_sf + (size_t)h * Np * C, Np, d, fmt, Kd);
+    oracle_dequant_fmt(v_codes + (size_t)h * Np * d, v_sf + (size_t)h * d * (Np / G), d, Np, fmt, Vt);
     const float* qm_h = q_mean ? q_mean + (size_t)h * (Np / 128) * d : NULL;
     const float* ks_h = ks ? ks + (size_t)h * Np * d : NULL;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int r = 0; r < nrows; ++r) {
       int qi = rows[r];
       attn_row(&Qd[(size_t)qi * d], Kd, Vt, N, Np, d, Bkv, causal, qi, scale, p_mode,
-               qm_h ? qm_h + (size_t)(qi / 128) * d : NULL, ks_h, &O[((size_t)h * nrows + r) * d],
+               qm_h ? qm_h + (size_t)(qi / 128) * d : NULL, ks_h, fmt, &O[((size_t)h * nrows + r) * d],
                lse ? &lse[(size_t)h * nrows + r] : NULL);
     }
     free(Qd);
     free(Kd);
     free(Vt);
   }
+}
+
+EXPORT void oracle_attn_fwd_sq(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
+                               const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
+                               const uint8_t* v_sf, const float* q_mean, const float* ks, int Bkv, int causal,
+                               double scale, int p_mode, const int* rows, int nrows, double* O, double* lse) {
+  oracle_attn_fwd_fmt(BH, N, d, q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, q_mean, ks, 0, Bkv, causal, scale, p_mode,
+                      rows, nrows, O, lse);
 }
 
 EXPORT void oracle_attn_fwd(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
@@ -465,7 +505,7 @@ EXPORT void oracle_attn_fwd_float(int N, int d, const float* Q, const float* K, 
   for (int r = 0; r < nrows; ++r) {
     double* Qrow = (double*)malloc(sizeof(double) * (size_t)d);
     for (int c = 0; c < d; ++c) Qrow[c] = Q[(size_t)rows[r] * d + c];
-    attn_row(Qrow, Kd, Vt, N, Np, d, Bkv, causal, rows[r], scale, p_mode, NULL, NULL, &O[(size_t)r * d],
+    attn_row(Qrow, Kd, Vt, N, Np, d, Bkv, causal, rows[r], scale, p_mode, NULL, NULL, 0, &O[(size_t)r * d],
              lse ? &lse[r] : NULL);
     free(Qrow);
   }
