@@ -47,6 +47,13 @@ typedef enum {
 
 typedef enum { SAGE3_FP16 = 0, SAGE3_BF16 = 1, SAGE3_FP32 = 2 /* output only */ } sage3_dtype;
 
+/* FP4 microscaling format of Q̂, K̂, V̂ and P̂2.  NVFP4 is the method; MXFP4 is the data-type
+ * ablation of Tab1a, kept as a switch for the accuracy / throughput comparison. */
+typedef enum {
+  SAGE3_NVFP4 = 0, /* E2M1 codes, UE4M3 scale per 16 elements (tcgen05 scale_vec::4X)                    */
+  SAGE3_MXFP4 = 1  /* E2M1 codes, UE8M0 scale 2^(e-127) per 32 elements (tcgen05 scale_vec::2X)          */
+} sage3_fp4_format;
+
 /* A [B][H][N][d] tensor: element (b,h,n,c) is at ptr + b*stride_b + h*stride_h + n*stride_n + c
  * (strides in ELEMENTS; the d stride is 1).  ptr and every stride*sizeof(elem) must be 16-byte aligned. */
 typedef struct {
@@ -54,15 +61,17 @@ typedef struct {
   int64_t stride_b, stride_h, stride_n;
 } sage3_tensor4;
 
-/* NVFP4 Q, K, V of one call, produced by sage3_quantize_qkv and consumed by sage3_attn_fwd.
- * N_pad = round_up(N, 128).  Codes: E2M1, two per byte, element 2k in the LOW nibble.
- *   q_data, k_data : [B][H][N_pad][d/2]     blocks of 16 along d (the QK^T reduction dim)
- *   v_data         : [B][H][d][N_pad/2]     V transposed: tokens contiguous, blocks of 16 tokens
- * Scales: E4M3 (UE4M3, sign 0), one per 16-element block, in 512-byte SF atoms of 128 rows x 4 blocks:
- *   byte(r, c) = ((r/128)*(C/4) + c/4)*512 + (r%32)*16 + ((r/32)%4)*4 + (c%4)      per (b,h) matrix
- *   q_sf, k_sf : R = N_pad rows (tokens), C = d/16 blocks;       N_pad*d/16 bytes per (b,h)
- *   v_sf       : R = 128 rows (channels, rows >= d are zero), C = N_pad/16;  8*N_pad bytes per (b,h)
- *   (the layout tcgen05.cp.32x128b.warpx4 expects; identical to cuBLAS's VEC16_UE4M3 layout)
+/* FP4 Q, K, V of one call, produced by sage3_quantize_qkv and consumed by sage3_attn_fwd.
+ * N_pad = round_up(N, 128).  fmt: a sage3_fp4_format, set by the caller before sage3_quantize_qkv (G = 16
+ * for NVFP4, 32 for MXFP4).  Codes: E2M1, two per byte, element 2k in the LOW nibble.
+ *   q_data, k_data : [B][H][N_pad][d/2]     blocks of G along d (the QK^T reduction dim)
+ *   v_data         : [B][H][d][N_pad/2]     V transposed: tokens contiguous, blocks of G tokens
+ * Scales: one byte per G-element block (NVFP4: UE4M3; MXFP4: UE8M0), in 512-byte SF atoms of 128 rows x 4
+ * blocks (C4 = round_up(C, 4) columns; columns >= C are zero):
+ *   byte(r, c) = ((r/128)*(C4/4) + c/4)*512 + (r%32)*16 + ((r/32)%4)*4 + (c%4)      per (b,h) matrix
+ *   q_sf, k_sf : R = N_pad rows (tokens), C = d/G blocks       NVFP4: N_pad*d/16, MXFP4: 4*N_pad bytes per (b,h)
+ *   v_sf       : R = 128 rows (channels, rows >= d are zero), C = N_pad/G   NVFP4: 8*N_pad, MXFP4: 4*N_pad
+ *   (the layout tcgen05.cp.32x128b.warpx4 expects; identical to cuBLAS's VEC16_UE4M3 / VEC32_UE8M0 layouts)
  * Padding tokens n in [N, N_pad) hold zero codes and zero scales.
  *   k_mean : [B][H][d] fp32, the smoothing-K mean (Alg1 L2).
  * Smoothing Q (Alg1 L5 + the GEMV of L8; off on the north_star path): set q_mean and ds non-null.
@@ -73,6 +82,7 @@ typedef struct {
  *   Both NULL = no smoothing Q (the north_star path).  Sizes: sage3_smooth_q_sizes(). */
 typedef struct {
   int32_t B, H, N, d, N_pad;
+  int32_t fmt; /* sage3_fp4_format; 0 (NVFP4) when the struct is zero-initialised */
   uint8_t* q_data;
   uint8_t* k_data;
   uint8_t* v_data;
@@ -85,8 +95,10 @@ typedef struct {
 } sage3_fp4_qkv;
 
 /* Host-only size queries (no CUDA calls).  bytes[0..6] = q_data, k_data, v_data, q_sf, k_sf, v_sf,
- * k_mean.  Returns SAGE3_ERR_INVALID_ARG for unsupported shapes. */
+ * k_mean of the NVFP4 format (sage3_fp4_qkv_sizes) or of `fmt` (sage3_fp4_qkv_sizes_fmt).  Returns
+ * SAGE3_ERR_INVALID_ARG for unsupported shapes or formats. */
 sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]);
+sage3_status sage3_fp4_qkv_sizes_fmt(int B, int H, int N, int d, int fmt, size_t bytes[7]);
 
 /* Host-only size queries for smoothing Q: bytes[0] = q_mean, bytes[1] = ds (see sage3_fp4_qkv). */
 sage3_status sage3_smooth_q_sizes(int B, int H, int N, int d, size_t bytes[2]);
@@ -108,16 +120,18 @@ int sage3_kv_tile(int d);
  * NaN/Inf (the codes are then unspecified).
  * Numerics (bit-exact with oracle_quantize_head): km[c] = fl32(Σ_chunks Σ_tokens K / N) in fp64 with the
  * fixed order of DESIGN.md reading c10; x = fl32(K - km); s = E4M3_RNE(fl32(amax·fl32(1/6)));
- * codes = E2M1_RNE(fl32(x·fl32(1/s))), all-zero codes when s == 0. */
+ * codes = E2M1_RNE(fl32(x·fl32(1/s))), all-zero codes when s == 0.  MXFP4 (out->fmt = SAGE3_MXFP4, Tab1a):
+ * s = the smallest power of two >= fl32(amax·fl32(1/6)) (reading c11), code = E2M1_RNE(x / s) (exact
+ * scaling), scale byte 0 and zero codes when amax·fl32(1/6) == 0. */
 sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 v, sage3_dtype in_dtype, int B,
                                 int H, int N, int d, sage3_fp4_qkv* out, void* workspace, size_t workspace_bytes,
                                 uint32_t* nonfinite_flag, void* stream);
 
-/* Alg1 L6-L13 on the NVFP4 tensors of *qkv.  o: [B][H][N][d] in o_dtype (FP16, BF16 or FP32); rows
+/* Alg1 L6-L13 on the FP4 tensors of *qkv (NVFP4, or MXFP4 with 32-key P̂2 blocks and UE8M0 s_P2).  o: [B][H][N][d] in o_dtype (FP16, BF16 or FP32); rows
  * n >= N are never written.  causal != 0: key j is visible to query i iff j <= i (top-left aligned).
  * softmax_scale <= 0 selects 1/sqrt(d); S is scaled after the MMA: P̃ = exp(scale·(S - m)).
  * lse: nullable device fp32 [B][H][N], lse = scale·m + ln(l) (natural log).
- * The tensor-core path: tcgen05.mma.kind::mxf4nvf4.block_scale (scale_vec::4X) for QK^T and PV with
+ * The tensor-core path: tcgen05.mma.kind::mxf4nvf4.block_scale (scale_vec::4X; 2X for MXFP4) for QK^T and PV with
  * fp32 accumulators and scale factors in TMEM, TMA-staged operands, B_q = B_kv = 128. */
 sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
                             float softmax_scale, float* lse, void* stream);

@@ -18,11 +18,13 @@ LIB_PATH = os.environ.get("SAGE3_LIB") or os.path.join(PKG, "libsage3.so")  # en
 
 SAGE3_OK, SAGE3_ERR_INVALID_ARG, SAGE3_ERR_UNSUPPORTED, SAGE3_ERR_WORKSPACE, SAGE3_ERR_CUDA = range(5)
 SAGE3_FP16, SAGE3_BF16, SAGE3_FP32 = 0, 1, 2
+SAGE3_NVFP4, SAGE3_MXFP4 = 0, 1  # sage3_fp4_format: the method / the Tab1a data-type ablation
+_FMT = {"nvfp4": SAGE3_NVFP4, "mxfp4": SAGE3_MXFP4, SAGE3_NVFP4: SAGE3_NVFP4, SAGE3_MXFP4: SAGE3_MXFP4}
 _DT = {torch.float16: SAGE3_FP16, torch.bfloat16: SAGE3_BF16, torch.float32: SAGE3_FP32}
 
 # Every function include/sage3.h declares (checked by tests/test_abi.py).
 ABI_FUNCTIONS = (
-    "sage3_fp4_qkv_sizes", "sage3_smooth_q_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
+    "sage3_fp4_qkv_sizes", "sage3_fp4_qkv_sizes_fmt", "sage3_smooth_q_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
     "sage3_attn_fwd", "sage3_attn_fwd_units", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
     "sage3_last_cuda_error", "sage3_version",
 )
@@ -39,7 +41,7 @@ class Tensor4(ctypes.Structure):
 
 class FP4QKVStruct(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("N", ctypes.c_int32), ("d", ctypes.c_int32),
-                ("N_pad", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in (
+                ("N_pad", ctypes.c_int32), ("fmt", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in (
                     "q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean", "q_mean", "ds")]
 
 
@@ -57,6 +59,7 @@ def load() -> ctypes.CDLL:
     L = ctypes.CDLL(LIB_PATH)
     sz = ctypes.c_size_t
     L.sage3_fp4_qkv_sizes.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(sz)]
+    L.sage3_fp4_qkv_sizes_fmt.argtypes = [ctypes.c_int] * 5 + [ctypes.POINTER(sz)]
     L.sage3_smooth_q_sizes.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(sz)]
     L.sage3_quantize_workspace_bytes.argtypes = [ctypes.c_int] * 4
     L.sage3_quantize_workspace_bytes.restype = sz
@@ -114,6 +117,12 @@ def sage3_fp4_qkv_sizes(B: int, H: int, N: int, d: int) -> list[int]:
     return list(out)
 
 
+def sage3_fp4_qkv_sizes_fmt(B: int, H: int, N: int, d: int, fmt) -> list[int]:
+    out = (ctypes.c_size_t * 7)()
+    _check(load().sage3_fp4_qkv_sizes_fmt(B, H, N, d, _FMT.get(fmt, -1), out), "sage3_fp4_qkv_sizes_fmt")
+    return list(out)
+
+
 def sage3_smooth_q_sizes(B: int, H: int, N: int, d: int) -> list[int]:
     out = (ctypes.c_size_t * 2)()
     _check(load().sage3_smooth_q_sizes(B, H, N, d, out), "sage3_smooth_q_sizes")
@@ -125,15 +134,19 @@ def sage3_quantize_workspace_bytes(B: int, H: int, N: int, d: int) -> int:
 
 
 class FP4QKV:
-    """Device buffers of one NVFP4 Q/K/V set (layouts: include/sage3.h), allocated with torch."""
+    """Device buffers of one FP4 Q/K/V set (layouts: include/sage3.h), allocated with torch.
+    fmt: "nvfp4" (the method) or "mxfp4" (Tab1a ablation)."""
 
     NAMES = ("q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean")
 
-    def __init__(self, B: int, H: int, N: int, d: int, device, smooth_q: bool = False):
+    def __init__(self, B: int, H: int, N: int, d: int, device, smooth_q: bool = False, fmt="nvfp4"):
         self.B, self.H, self.N, self.d = B, H, N, d
         self.N_pad = (N + 127) // 128 * 128
         self.smooth_q = smooth_q
-        sizes = sage3_fp4_qkv_sizes(B, H, N, d)
+        if fmt not in _FMT:
+            raise Sage3Error(f"unknown FP4 format {fmt!r}")
+        self.fmt = _FMT[fmt]
+        sizes = sage3_fp4_qkv_sizes_fmt(B, H, N, d, self.fmt)
         for name, nbytes in zip(self.NAMES, sizes):
             setattr(self, name, torch.empty(nbytes, dtype=torch.uint8, device=device))
         self.q_mean = self.ds = None
@@ -143,7 +156,7 @@ class FP4QKV:
             self.ds = torch.empty(ds_b, dtype=torch.uint8, device=device)
         self.workspace = torch.empty(max(sage3_quantize_workspace_bytes(B, H, N, d), 16), dtype=torch.uint8,
                                      device=device)
-        self.struct = FP4QKVStruct(B, H, N, d, self.N_pad,
+        self.struct = FP4QKVStruct(B, H, N, d, self.N_pad, self.fmt,
                                    *[getattr(self, n).data_ptr() for n in self.NAMES],
                                    self.q_mean.data_ptr() if smooth_q else None,
                                    self.ds.data_ptr() if smooth_q else None)
@@ -153,12 +166,14 @@ class FP4QKV:
 
 
 def sage3_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: FP4QKV | None = None,
-                       nonfinite: torch.Tensor | None = None, stream=None, smooth_q: bool = False) -> FP4QKV:
-    """Alg1 L2 + L7 (smoothing K, NVFP4 φ of Q, K, V; + L5 / L8's GEMV with smooth_q): see include/sage3.h."""
+                       nonfinite: torch.Tensor | None = None, stream=None, smooth_q: bool = False,
+                       fmt="nvfp4") -> FP4QKV:
+    """Alg1 L2 + L7 (smoothing K, FP4 φ of Q, K, V; + L5 / L8's GEMV with smooth_q): see include/sage3.h.
+    The format of a given `out` is its own (fmt applies when out is None)."""
     B, H, N, d = q.shape
     assert k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dtype in (torch.float16, torch.bfloat16)
     if out is None:
-        out = FP4QKV(B, H, N, d, q.device, smooth_q=smooth_q)
+        out = FP4QKV(B, H, N, d, q.device, smooth_q=smooth_q, fmt=fmt)
     flag = ctypes.c_void_p(nonfinite.data_ptr() if nonfinite is not None else None)
     st = load().sage3_quantize_qkv(_t4(q), _t4(k), _t4(v), _DT[q.dtype], B, H, N, d, ctypes.byref(out.struct),
                                    ctypes.c_void_p(out.workspace.data_ptr()), out.workspace.numel(), flag,
@@ -215,9 +230,10 @@ def sage3_forward_host(q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch
 
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
-              softmax_scale: float = 0.0, out_dtype=None, stream=None, smooth_q: bool = False) -> torch.Tensor:
+              softmax_scale: float = 0.0, out_dtype=None, stream=None, smooth_q: bool = False,
+              fmt="nvfp4") -> torch.Tensor:
     """Quantize + attention in one call (the two ABI calls, enqueued on the current stream)."""
-    qkv = sage3_quantize_qkv(q, k, v, stream=stream, smooth_q=smooth_q)
+    qkv = sage3_quantize_qkv(q, k, v, stream=stream, smooth_q=smooth_q, fmt=fmt)
     return sage3_attn_fwd(qkv, causal=causal, softmax_scale=softmax_scale, out_dtype=out_dtype or q.dtype,
                           stream=stream)
 

@@ -80,17 +80,23 @@ Pipe* pipe_for_current_device() {
 
 extern "C" {
 
-sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]) {
-  if (!bytes || !shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
+sage3_status sage3_fp4_qkv_sizes_fmt(int B, int H, int N, int d, int fmt, size_t bytes[7]) {
+  if (!bytes || !shape_ok(B, H, N, d) || (fmt != SAGE3_NVFP4 && fmt != SAGE3_MXFP4)) return SAGE3_ERR_INVALID_ARG;
   const size_t BH = (size_t)B * H, Np = (size_t)npad(N);
+  const bool mx = fmt == SAGE3_MXFP4;
   bytes[0] = BH * Np * d / 2;   // q_data
   bytes[1] = BH * Np * d / 2;   // k_data
   bytes[2] = BH * d * Np / 2;   // v_data
-  bytes[3] = BH * Np * d / 16;  // q_sf
-  bytes[4] = BH * Np * d / 16;  // k_sf
-  bytes[5] = BH * 128 * Np / 16;  // v_sf (128 channel rows, zero beyond d)
+  // SF atoms: 512 bytes per 128 rows x 4 blocks; MXFP4 (d/32 <= 4 blocks per row) fills one atom column group
+  bytes[3] = mx ? BH * Np * 4 : BH * Np * d / 16;  // q_sf
+  bytes[4] = bytes[3];                              // k_sf
+  bytes[5] = mx ? BH * Np * 4 : BH * 128 * Np / 16;  // v_sf (128 channel rows, zero beyond d)
   bytes[6] = BH * d * sizeof(float);  // k_mean
   return SAGE3_OK;
+}
+
+sage3_status sage3_fp4_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]) {
+  return sage3_fp4_qkv_sizes_fmt(B, H, N, d, SAGE3_NVFP4, bytes);
 }
 
 sage3_status sage3_smooth_q_sizes(int B, int H, int N, int d, size_t bytes[2]) {
@@ -115,6 +121,7 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   if (in_dtype != SAGE3_FP16 && in_dtype != SAGE3_BF16) return SAGE3_ERR_UNSUPPORTED;
   if (!tensor_ok(q, 2) || !tensor_ok(k, 2) || !tensor_ok(v, 2)) return SAGE3_ERR_INVALID_ARG;
   if (out->B != B || out->H != H || out->N != N || out->d != d) return SAGE3_ERR_INVALID_ARG;
+  if (out->fmt != SAGE3_NVFP4 && out->fmt != SAGE3_MXFP4) return SAGE3_ERR_INVALID_ARG;
   if (!out->q_data || !out->k_data || !out->v_data || !out->q_sf || !out->k_sf || !out->v_sf || !out->k_mean)
     return SAGE3_ERR_INVALID_ARG;
   if (!aligned16(out->q_data) || !aligned16(out->k_data) || !aligned16(out->v_data) || !aligned16(out->q_sf) ||
@@ -136,6 +143,7 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   qa.k_mean = out->k_mean;
   qa.q_mean = out->q_mean;
   qa.ds = out->ds;
+  qa.mx = out->fmt == SAGE3_MXFP4;
   qa.nonfinite = nonfinite_flag;
   sage3::VArgs va{};
   va.v = v.ptr;
@@ -153,6 +161,7 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
                                   void* stream) {
   if (!qkv || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
   if (qkv->N_pad != npad(qkv->N)) return SAGE3_ERR_INVALID_ARG;
+  if (qkv->fmt != SAGE3_NVFP4 && qkv->fmt != SAGE3_MXFP4) return SAGE3_ERR_INVALID_ARG;
   const int64_t n_units = (int64_t)qkv->B * qkv->H * (qkv->N_pad / 128);
   if (unit_begin < 0 || unit_end < unit_begin || unit_end > n_units || unit_end - unit_begin > 0x7FFFFFFF)
     return SAGE3_ERR_INVALID_ARG;
@@ -170,6 +179,7 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
   if (st != SAGE3_OK) return st;
   sage3::AttnArgs a{};
   a.ds = qkv->ds;
+  a.mx = qkv->fmt == SAGE3_MXFP4;
   a.q_data = qkv->q_data, a.k_data = qkv->k_data, a.v_data = qkv->v_data;
   a.q_sf = qkv->q_sf, a.k_sf = qkv->k_sf, a.v_sf = qkv->v_sf;
   a.o = o.ptr, a.o_sb = o.stride_b, a.o_sh = o.stride_h, a.o_sn = o.stride_n, a.o_dtype = (int)o_dtype;

@@ -78,7 +78,7 @@ constexpr float kLog2_2688 = 11.392317422778761f;  // log2(448 * 6)
 constexpr int kSBufs = 3;
 constexpr uint32_t kColSFQ = 384, kColSFK = 392, kColSFV = 400, kColSFP = 408;
 
-template <int D>
+template <int D, bool kMX>
 struct Layout {
   static constexpr int kQKRow = D / 2;          // bytes per Q/K row (64 or 32)
   static constexpr int kQBytes = 128 * kQKRow;   // Q tile codes
@@ -86,8 +86,10 @@ struct Layout {
   static constexpr int kKSlot = ((kKBytes + 1023) / 1024) * 1024;
   static constexpr int kVBytes = D * 64;    // Vᵀ tile: D channel rows x 128 tokens (64 B)
   static constexpr int kPBytes = 128 * 64;  // P̂2 tile: 128 rows x 128 keys (64 B)
-  static constexpr int kQKSF = (D / 64) * 512;     // SF atoms per 128-row tile along d
-  static constexpr int kVSF = 1024, kPSF = 1024;   // 8 token blocks = 2 atoms
+  // SF atoms per 128-row tile: NVFP4 d/16 blocks along d (1 or 2 atoms), 8 token blocks (2 atoms);
+  // MXFP4 d/32 <= 4 blocks along d and 4 token blocks (1 atom each)
+  static constexpr int kQKSF = kMX ? 512 : (D / 64) * 512;
+  static constexpr int kVSF = kMX ? 512 : 1024, kPSF = kVSF;
   // byte offsets inside the 1024-aligned dynamic smem window
   static constexpr int oQ = 0;
   static constexpr int oK = oQ + ((kQBytes + 1023) / 1024) * 1024;
@@ -217,11 +219,13 @@ __device__ unsigned long long g_trace[2][8][128][8];
   } while (0)
 #endif
 
-template <int D, bool kSQ>  // kSQ: smoothing Q (S += ds, Alg1 L8's GEMV term)
+// kSQ: smoothing Q (S += ds, Alg1 L8's GEMV term).  kMX: MXFP4 operands (Tab1a ablation): scale_vec::2X MMAs
+// with UE8M0 scales, P̂2 in 32-key blocks whose scale is the smallest power of two >= amax/6 (reading c11).
+template <int D, bool kSQ, bool kMX>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const AttnArgs a) {
-  using L = Layout<D>;
+  using L = Layout<D, kMX>;
   extern __shared__ uint8_t smem_raw[];
   // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
   __shared__ __align__(1024) float2 s_lut[128];
@@ -309,14 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row_q = bh * a.Np + qt * 128;
         mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
         tma_load_2d(sQ, &tm_q, q_full, 0, row_q);
-        bulk_load(sQSF, a.q_sf + (int64_t)row_q * (D / 16), L::kQKSF, q_full);
+        bulk_load(sQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
         for (int j = 0; j < nkv; ++j) {
           const int st = j % kKStages;
           const int row_k = bh * a.Np + j * 128;
           mbar_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
           tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
-          bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)row_k * (D / 16), L::kQKSF, &k_full[st]);
+          bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
+                    &k_full[st]);
         }
       }
       __syncwarp();
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
           tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
-          bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + (int64_t)bh * 128 * (a.Np / 16) + j * 1024, L::kVSF,
+          bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
                     &v_full[st]);
         }
       }
@@ -346,8 +351,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // its own completions)
       if (elect_one()) {
         constexpr uint32_t kQKLayout = D == 128 ? kLayoutSw64 : kLayoutSw32;
-        constexpr uint32_t idesc_s = make_idesc_nvf4(128, 128);
-        constexpr uint32_t idesc_pv = make_idesc_nvf4(128, D);
+        constexpr int kQKAtoms = L::kQKSF / 512, kPVAtoms = L::kPSF / 512;
+        // one K-step (64 elements) of a block-scaled FP4 MMA: NVFP4 reads scale columns sf + 4ks; MXFP4 reads
+        // bytes 2ks, 2ks+1 of column sf (sf id in the instruction descriptor)
+        auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t n, int ks, uint32_t sfa, uint32_t sfb) {
+          if constexpr (kMX)
+            mma_mxf4(d, ad, bd, make_idesc_mxf4(128, n, ks), sfa, sfb, ks > 0);
+          else
+            mma_nvf4(d, ad, bd, make_idesc_nvf4(128, n), sfa + 4 * ks, sfb + 4 * ks, ks > 0);
+        };
         auto issue_s = [&](int j) {
           const int b = j % kSBufs, st = j % kKStages;
           SAGE3_TRACE_EV(5, j, 0);
@@ -359,12 +371,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint8_t* sK = smem + L::oK + st * L::kKSlot;
           const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
 #pragma unroll
-          for (int ks = 0; ks < D / 64; ++ks) tmem_cp_32x128b_x4(tbase + kColSFK + 4 * ks, sf_desc(sKSF + 512 * ks));
+          for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFK + 4 * at, sf_desc(sKSF + 512 * at));
 #pragma unroll
           for (int ks = 0; ks < D / 64; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sQ) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
             const uint64_t bd = make_smem_desc(smem_u32(sK) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
-            mma_nvf4(tbase + 128 * b, ad, bd, idesc_s, tbase + kColSFQ + 4 * ks, tbase + kColSFK + 4 * ks, ks > 0);
+            mma(tbase + 128 * b, ad, bd, 128, ks, tbase + kColSFQ, tbase + kColSFK);
           }
           mma_commit(&k_empty[st]);
           mma_commit(&s_full[b]);
@@ -383,15 +395,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint8_t* sPSF = smem + L::oPSF + pb * L::kPSF;
           const uint8_t* sVSF = smem + L::oVSF + st * L::kVSF;
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            tmem_cp_32x128b_x4(tbase + kColSFP + 4 * ks, sf_desc(sPSF + 512 * ks));
-            tmem_cp_32x128b_x4(tbase + kColSFV + 4 * ks, sf_desc(sVSF + 512 * ks));
+          for (int at = 0; at < kPVAtoms; ++at) {
+            tmem_cp_32x128b_x4(tbase + kColSFP + 4 * at, sf_desc(sPSF + 512 * at));
+            tmem_cp_32x128b_x4(tbase + kColSFV + 4 * at, sf_desc(sVSF + 512 * at));
           }
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sP) + 32 * ks, 16, 512, kLayoutSw64);
             const uint64_t bd = make_smem_desc(smem_u32(sV) + 32 * ks, 16, 512, kLayoutSw64);
-            mma_nvf4(tbase + 128 * b, ad, bd, idesc_pv, tbase + kColSFP + 4 * ks, tbase + kColSFV + 4 * ks, ks > 0);
+            mma(tbase + 128 * b, ad, bd, D, ks, tbase + kColSFP, tbase + kColSFV);
           }
           mma_commit(&v_empty[st]);
           mma_commit(&p_empty[pb]);
@@ -402,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(q_full, 0);
           tc_fence_after();
 #pragma unroll
-          for (int ks = 0; ks < D / 64; ++ks) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * ks, sf_desc(sQSF + 512 * ks));
+          for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * at, sf_desc(sQSF + 512 * at));
           for (int j = 0; j < nkv; ++j) issue_s(j);  // S_j into buffer j%3 once the correction freed it
         } else {
           for (int j = 0; j < nkv; ++j) issue_pv(j);
@@ -502,8 +514,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       //      PV MMA multiplies them by s = 0, so they contribute exactly 0, as the oracle's zero codes do;
       //      its table entry (10, 2^-10) keeps its unquantized P̃2 in the row sum (reading c9).
       float nbb[8], sdec[8];
-      uint32_t scw[2];
-      {
+      uint32_t scw[2] = {0u, 0u};
+      if constexpr (kMX) {
+        // MXFP4: 32-key blocks (block k = keys [32k, 32k+32) = pass-2 chunk k), s = 2^p the smallest power of two
+        // >= fl32(amax/6) (UE8M0 code p + 127), so -log2 s = -p exactly.  amax/6 == 0: scale byte 0, and the
+        // (10, 2^-10) substitute of the NVFP4 zero scale keeps pass 2 finite (its codes are 0 there anyway).
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float bm = fmaxf(bmax[2 * k], bmax[2 * k + 1]);
+          const float s32 = __fmul_rn(ex2(fmaf(bm, sl2, nb)), kOneSixth);
+          float rs;
+          const uint32_t code = e8m0_ceil(s32, rs);
+          const bool z = s32 == 0.0f;
+          scw[0] |= (z ? 0u : code) << (8 * k);
+          nbb[2 * k] = nbb[2 * k + 1] = z ? nb + 10.0f : nb + (127.0f - (float)code);
+          sdec[2 * k] = sdec[2 * k + 1] = z ? 0x1p-10f : e8m0_to_f32(code);
+        }
+      } else {
         uint32_t c2[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -578,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         finish(3, yb);
       }
       sts_u32(sPSF, scw[0]);
-      sts_u32(sPSF + 512, scw[1]);
+      if constexpr (!kMX) sts_u32(sPSF + 512, scw[1]);
       const int slot = j % kXSlots;
       sts_f32(xchg_s + slot * 1024, tmax);
       sts_f32(xchg_s + slot * 1024 + 512, rowsum);
@@ -731,14 +758,14 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, bool kSQ>
+template <int D, bool kSQ, bool kMX>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D>;
+  using L = Layout<D, kMX>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
@@ -750,15 +777,20 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_fwd_kernel<D, kSQ><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
+  attn_fwd_kernel<D, kSQ, kMX><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+template <bool kMX>
+cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
+  if (a.ds) return a.d == 128 ? launch_d<128, true, kMX>(a, stream) : launch_d<64, true, kMX>(a, stream);
+  return a.d == 128 ? launch_d<128, false, kMX>(a, stream) : launch_d<64, false, kMX>(a, stream);
+}
+
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream) {
-  if (a.ds) return a.d == 128 ? launch_d<128, true>(a, stream) : launch_d<64, true>(a, stream);
-  return a.d == 128 ? launch_d<128, false>(a, stream) : launch_d<64, false>(a, stream);
+  return a.mx ? launch_fmt<true>(a, stream) : launch_fmt<false>(a, stream);
 }
 
 #ifdef SAGE3_TRACE

@@ -16,6 +16,7 @@ struct QKArgs {
   float* k_mean;  // written by the K-mean pass, read by quant_qk
   float* q_mean;  // smoothing Q (nullable): [B][H][Np/128][d]
   float* ds;      // smoothing Q (nullable): [B][H][Np/128][Np] GEMV(q̄_i, K^T)
+  bool mx;        // MXFP4 (Tab1a ablation): E8M0 scales per 32 instead of E4M3 per 16
   uint32_t* nonfinite;
 };
 
@@ -40,6 +41,7 @@ struct AttnArgs {
   int causal;
   float scale;  // softmax scale (S units)
   const float* ds;  // smoothing Q (nullable): [B][H][Np/128][Np], added to S
+  bool mx;          // MXFP4 operands (scale_vec::2X MMAs, 32-key P̂2 blocks with E8M0 scales)
   int64_t unit_begin, unit_end;  // work units [begin, end) of the flattened (b·h, q-tile) space
 };
 

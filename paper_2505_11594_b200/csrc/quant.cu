@@ -3,6 +3,7 @@
 // transposed).  HBM-bound: K-mean sums (4-byte coalesced loads, fp64) + their fixed-order reduction,
 // then one persistent streaming kernel (TMA tiles -> smem ring -> φ) over all Q, Vᵀ and K chunks.
 //
+// MXFP4 (Tab1a ablation, template kMX): blocks of 32 with E8M0 scales (e8m0_ceil in sm100.cuh, reading c11).
 // Numerics are the DESIGN.md §3 readings, implemented with explicitly rounded intrinsics so that no FMA
 // contraction or fast-math can change a bit:
 //   km[c] = fl32( (Σ_chunk Σ_token K[n][c]) / N ) in fp64, chunks of 128 tokens, ascending order (c10)
@@ -167,7 +168,7 @@ struct QL {
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-template <typename T, int D>
+template <typename T, int D, bool kMX>
 __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                               const __grid_constant__ CUtensorMap tm_k,
                                                               const __grid_constant__ CUtensorMap tm_v, QKArgs qa,
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
     }
     fence_mbar_init();
   }
-  for (int i = t; i < 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm + L::oSFv)[i] = make_uint4(0, 0, 0, 0);
+  // SF staging starts zeroed: atom rows (Vᵀ channels >= d) and MXFP4 columns (d/32 < 4) never written stay 0
+  for (int i = t; i < 2048 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm + L::oSFqk)[i] = make_uint4(0, 0, 0, 0);
   if (t < 128) {
     const float sd = e4m3_to_f32((uint32_t)t);
     s_rcp[t] = (sd == 0.0f || t == 0x7F) ? 0.0f : __frcp_rn(sd);
@@ -262,29 +264,74 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
         }
         float amax = amax8(x);
         amax = fmax3_nan(amax, __shfl_xor_sync(0xffffffffu, amax, 1), 0.0f);
+        if constexpr (kMX) amax = fmax3_nan(amax, __shfl_xor_sync(0xffffffffu, amax, 2), 0.0f);  // 32-blocks
         finite &= isfinite(amax);
         // padding rows (n >= N) arrive as zeros from TMA; they must stay zero codes / zero scales even
         // after smoothing (reading c13)
         const bool real = chunk * 128 + r < qa.N;
-        const uint32_t sc = real ? cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu : 0u;
-        // a zero scale gives all-zero codes (c5; x·0 would keep the sign of x: E2M1 -0 = 0x8)
-        const uint32_t w = sc ? codes8(x, s_rcp[sc]) : 0u;
+        uint32_t sc, w;
+        if constexpr (kMX) {
+          const float s32 = __fmul_rn(amax, kOneSixth);
+          float rs;
+          sc = e8m0_ceil(s32, rs);
+          const bool nz = real && s32 != 0.0f;  // amax = 0: scale byte 0 with zero codes (reading c11)
+          sc = nz ? sc : 0u;
+          w = nz ? codes8(x, rs) : 0u;
+        } else {
+          sc = real ? cvt_e4m3x2(__fmul_rn(amax, kOneSixth), 0.0f) & 0xFFu : 0u;
+          // a zero scale gives all-zero codes (c5; x·0 would keep the sign of x: E2M1 -0 = 0x8)
+          w = sc ? codes8(x, s_rcp[sc]) : 0u;
+        }
         *reinterpret_cast<uint32_t*>(codes + r * (D / 2) + cv * 4) = w;
-        if ((cv & 1) == 0) {
-          const int c = cv >> 1;
+        constexpr int kPer = kMX ? 4 : 2;  // threads per scale block
+        if ((cv & (kPer - 1)) == 0) {
+          const int c = cv / kPer;
           sfs[(c >> 2) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (c & 3)] = (uint8_t)sc;
         }
       }
       __syncwarp();
       if ((t & 31) == 0) mbar_arrive(&empty[s]);  // tile consumed
       consumer_bar();                             // SF staging complete
-      uint8_t* sf_dst = (smooth ? qa.k_sf : qa.q_sf) + (int64_t)bh * qa.Np * (D / 16) + (int64_t)chunk * 512 * (D / 64);
-      for (int i = t * 16; i < 512 * (D / 64); i += 256 * 16)
+      constexpr int kSFqk = kMX ? 512 : 512 * (D / 64);  // SF bytes of one 128-row tile
+      uint8_t* sf_dst = (smooth ? qa.k_sf : qa.q_sf) + ((int64_t)bh * nch + chunk) * kSFqk;
+      for (int i = t * 16; i < kSFqk; i += 256 * 16)
         *reinterpret_cast<uint4*>(sf_dst + i) = *reinterpret_cast<const uint4*>(sfs + i);
       consumer_bar();  // staging free for the next item
     } else {  // Vᵀ: φ along tokens
       uint8_t* vcode = sm + L::oVcode;
       uint8_t* sfs = sm + L::oSFv;
+      if constexpr (kMX) {  // blocks of 32 tokens: (channel pair, 32-token block) per item
+        for (int it = t; it < (D / 2) * 4; it += 256) {
+          const int cp = it % (D / 2), tb = it / (D / 2);
+          float x0[32], x1[32];
+          const uint32_t* col = reinterpret_cast<const uint32_t*>(tile) + tb * 32 * (D / 2) + cp;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const uint32_t u = col[e * (D / 2)];
+            const T* p = reinterpret_cast<const T*>(&u);
+            x0[e] = to_f32<T>(p[0]);
+            x1[e] = to_f32<T>(p[1]);
+          }
+          const int c = 2 * cp;
+          const float a0 = fmax3_nan(fmax3_nan(amax8(x0), amax8(x0 + 8), amax8(x0 + 16)), amax8(x0 + 24), 0.0f);
+          const float a1 = fmax3_nan(fmax3_nan(amax8(x1), amax8(x1 + 8), amax8(x1 + 16)), amax8(x1 + 24), 0.0f);
+          finite &= isfinite(a0) & isfinite(a1);
+          const float s0 = __fmul_rn(a0, kOneSixth), s1 = __fmul_rn(a1, kOneSixth);
+          float r0, r1;
+          uint32_t sc0 = e8m0_ceil(s0, r0), sc1 = e8m0_ceil(s1, r1);
+          sc0 = s0 != 0.0f ? sc0 : 0u;
+          sc1 = s1 != 0.0f ? sc1 : 0u;
+          *reinterpret_cast<uint4*>(vcode + c * 64 + tb * 16) =
+              s0 != 0.0f ? make_uint4(codes8(x0, r0), codes8(x0 + 8, r0), codes8(x0 + 16, r0), codes8(x0 + 24, r0))
+                         : make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(vcode + (c + 1) * 64 + tb * 16) =
+              s1 != 0.0f ? make_uint4(codes8(x1, r1), codes8(x1 + 8, r1), codes8(x1 + 16, r1), codes8(x1 + 24, r1))
+                         : make_uint4(0u, 0u, 0u, 0u);
+          const int base = ((c >> 5) & 3) * 4 + tb;  // one atom per chunk: 4 token blocks
+          sfs[base + (c & 31) * 16] = (uint8_t)sc0;
+          sfs[base + ((c + 1) & 31) * 16] = (uint8_t)sc1;
+        }
+      } else {
       for (int it = t; it < (D / 2) * 8; it += 256) {
         const int cp = it % (D / 2), tb = it / (D / 2);
         float x0[16], x1[16];
@@ -310,6 +357,7 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
         sfs[base + (c & 31) * 16] = (uint8_t)sc0;
         sfs[base + ((c + 1) & 31) * 16] = (uint8_t)sc1;
       }
+      }
       __syncwarp();
       if ((t & 31) == 0) mbar_arrive(&empty[s]);
       consumer_bar();
@@ -318,8 +366,9 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
         *reinterpret_cast<uint4*>(va.v_data + ((int64_t)bh * D + c) * (qa.Np >> 1) + chunk * 64 + q * 16) =
             *reinterpret_cast<const uint4*>(vcode + c * 64 + q * 16);
       }
-      uint8_t* sf_dst = va.v_sf + (int64_t)bh * 128 * (qa.Np >> 4) + (int64_t)chunk * 1024;
-      for (int i = t * 16; i < 1024; i += 256 * 16)
+      constexpr int kSFv = kMX ? 512 : 1024;  // SF bytes of one 128-token chunk (128 channel rows)
+      uint8_t* sf_dst = va.v_sf + ((int64_t)bh * nch + chunk) * kSFv;
+      for (int i = t * 16; i < kSFv; i += 256 * 16)
         *reinterpret_cast<uint4*>(sf_dst + i) = *reinterpret_cast<const uint4*>(sfs + i);
       consumer_bar();
     }
@@ -407,15 +456,15 @@ bool make_input_map(CUtensorMap* m, const void* base, int B, int H, int N, int d
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, int D>
+template <typename T, int D, bool kMX>
 cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t stream) {
   using L = QL<D>;
-  static bool attr_done[64] = {};
+  static bool attr_done[64] = {};  // per instantiation
   static int n_sm[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(quant_stream_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(quant_stream_kernel<T, D, kMX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          L::kAlloc);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
@@ -433,7 +482,7 @@ cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t 
   kmean_final_kernel<<<(BH * D * 32 + 255) / 256, 256, 0, stream>>>(ws, qk.Np / 128, qk.N, BH * D, qk.k_mean);
   const int items = 3 * BH * (qk.Np / 128);
   const int ctas = min(items, 2 * (dev < 64 && n_sm[dev] ? n_sm[dev] : 148));
-  quant_stream_kernel<T, D><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v);
+  quant_stream_kernel<T, D, kMX><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v);
   if (qk.q_mean) {  // smoothing Q: the GEMV term, after every q̄ of the head is written
     static bool ds_attr[64] = {};
     constexpr int kDsSmem = (D * 128 + D * 64) * 4;
@@ -449,12 +498,17 @@ cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t 
 
 }  // namespace
 
-cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream) {
+template <bool kMX>
+cudaError_t launch_fmt(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream) {
   if (qk.d == 128)
-    return bf16 ? launch_t<__nv_bfloat16, 128>(qk, v, ws, stream)
-                : launch_t<__half, 128>(qk, v, ws, stream);
-  return bf16 ? launch_t<__nv_bfloat16, 64>(qk, v, ws, stream)
-              : launch_t<__half, 64>(qk, v, ws, stream);
+    return bf16 ? launch_t<__nv_bfloat16, 128, kMX>(qk, v, ws, stream)
+                : launch_t<__half, 128, kMX>(qk, v, ws, stream);
+  return bf16 ? launch_t<__nv_bfloat16, 64, kMX>(qk, v, ws, stream)
+              : launch_t<__half, 64, kMX>(qk, v, ws, stream);
+}
+
+cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream) {
+  return qk.mx ? launch_fmt<true>(qk, v, bf16, ws, stream) : launch_fmt<false>(qk, v, bf16, ws, stream);
 }
 
 }  // namespace sage3

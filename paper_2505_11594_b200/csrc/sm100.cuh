@@ -142,6 +142,12 @@ __device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo_
 __host__ __device__ constexpr uint32_t make_idesc_nvf4(uint32_t M, uint32_t N) {
   return (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
+// MXFP4 (scale_vec::2X): [23] scale fmt = 1 (UE8M0); the two scale bytes of K-step ks (64 elements = 2 blocks
+// of 32) are bytes 2ks, 2ks+1 of the row's 4-byte SF column group: sf id = 2ks for B ([4,6)) and A ([29,31)).
+// (Measured on the B200: tools/probe_mx.cu, hypothesis 0.)
+__host__ __device__ constexpr uint32_t make_idesc_mxf4(uint32_t M, uint32_t N, uint32_t ks) {
+  return make_idesc_nvf4(M, N) | (1u << 23) | ((2u * ks) << 29) | ((2u * ks) << 4);
+}
 
 // ---------------------------------------------------------------- tcgen05: MMA / copy / commit
 // D[tmem] (+)= A[smem] x B[smem]^T with per-16-element E4M3 scales SFA/SFB in TMEM.
@@ -151,6 +157,17 @@ __device__ __forceinline__ void mma_nvf4(uint32_t d_tmem, uint64_t a_desc, uint6
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.scale_vec::4X [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
+// The same with per-32-element UE8M0 scales (MXFP4; idesc from make_idesc_mxf4).
+__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n\t"
       "}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
       : "memory");
@@ -272,6 +289,20 @@ __device__ __forceinline__ uint32_t cvt_e2m1x8(float a0, float a1, float a2, flo
   return r;
 }
 // packed e4m3x2 -> two halves (exact), used to decode a scale code.
+// MXFP4 scale (Tab1a ablation, reading c11): 2^p = the smallest power of two >= s32 (> 0, finite), p
+// clamped to [-127, 127] like the oracle; returns the UE8M0 code p + 127 and rs = 2^-p (x·rs = x / 2^p exactly).
+__device__ __forceinline__ uint32_t e8m0_ceil(float s32, float& rs) {
+  const uint32_t b = __float_as_uint(s32), e = b >> 23, m = b & 0x7FFFFFu;
+  // normal: 2^(e-127) if the mantissa is 0, else 2^(e-126); subnormal: 2^-126 above 2^-127, else 2^-127
+  const uint32_t code = e == 0 ? (m > 0x400000u ? 1u : 0u) : min(e + (m != 0u ? 1u : 0u), 254u);
+  rs = code < 254u ? __uint_as_float((254u - code) << 23) : 0x1p-127f;
+  return code;
+}
+// 2^(code - 127) of a UE8M0 code (code < 255)
+__device__ __forceinline__ float e8m0_to_f32(uint32_t code) {
+  return code ? __uint_as_float(code << 23) : 0x1p-127f;
+}
+
 __device__ __forceinline__ float e4m3_to_f32(uint32_t code) {
   uint32_t h2;
   uint16_t c = static_cast<uint16_t>(code & 0xFF);

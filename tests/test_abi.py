@@ -50,6 +50,13 @@ def test_size_queries(lib):
         s3.sage3_fp4_qkv_sizes(1, 1, 0, 64)
     with pytest.raises(s3.Sage3Error):
         s3.sage3_fp4_qkv_sizes(1, 1, 128, 96)
+    assert s3.sage3_fp4_qkv_sizes_fmt(B, H, N, d, "nvfp4") == sizes
+    # MXFP4: d/32 <= 4 scale columns -> one 512-byte atom per 128 rows for Q/K, 4 token blocks per V atom
+    for dd in (64, 128):
+        mx = s3.sage3_fp4_qkv_sizes_fmt(B, H, N, dd, "mxfp4")
+        assert mx == [B * H * Np * dd // 2] * 3 + [B * H * Np * 4] * 3 + [B * H * dd * 4]
+    with pytest.raises(s3.Sage3Error):
+        s3.sage3_fp4_qkv_sizes_fmt(B, H, N, d, 2)
 
 
 def test_invalid_arguments_rejected_before_any_cuda_call(lib):
@@ -63,6 +70,9 @@ def test_invalid_arguments_rejected_before_any_cuda_call(lib):
     f.N_pad = 128
     t = s3.Tensor4(16, 0, 0, 64)  # misaligned-free fake pointer, but the qkv buffers are null
     st = lib.sage3_attn_fwd(ctypes.byref(f), t, s3.SAGE3_BF16, 0, 0.0, None, None)
+    assert st == s3.SAGE3_ERR_INVALID_ARG
+    f.fmt = 7  # not a sage3_fp4_format
+    st = lib.sage3_quantize_qkv(t, t, t, s3.SAGE3_BF16, 1, 1, 128, 64, ctypes.byref(f), None, 0, None, None)
     assert st == s3.SAGE3_ERR_INVALID_ARG
     st = lib.sage3_forward_host(None, None, None, s3.SAGE3_BF16, 1, 1, 128, 64, 0, 0.0, None, s3.SAGE3_BF16, None, 0,
                                 None)
