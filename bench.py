@@ -124,7 +124,8 @@ def cpu_baseline(args, d, timeout_s=12.0):
     Q, K, V = (x.float().numpy() for x in (q, k, v))
     nthr = oracle.num_threads()
     t0 = time.perf_counter()
-    h = oracle.quantize_head(Q, K, V)
+    h = oracle.quantize_head(Q, K, V, fmt=oracle.FMT_MXFP4 if getattr(args, "fmt", "nvfp4") == "mxfp4" else
+                             oracle.FMT_NVFP4)
     tq = time.perf_counter() - t0
     # grow the row sample until one timed call takes about timeout_s (or covers all rows)
     R = max(4 * nthr, 16)
@@ -179,6 +180,8 @@ def workload_config(args, d):
     name = f"B=1,H={args.heads},N={args.n},d={d},{'causal' if args.causal else 'non-causal'}"
     if getattr(args, "smooth_q", False):
         name += ",smooth-q"
+    if getattr(args, "fmt", "nvfp4") != "nvfp4":
+        name += "," + args.fmt
     return {"workload": name, "B": 1, "H": args.heads, "N": args.n, "d": d, "causal": bool(args.causal),
             "per_rank": True, "parallelism": f"heads-sharded x{args.gpus}",
             "l2": "inputs larger than L2 (3 x %.0f MB bf16 vs 126 MB)" % (args.heads * args.n * d * 2 / 1e6)}
@@ -197,6 +200,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--smooth-q", action="store_true", help="Alg1 with smoothing Q (NEXT #1; off on the north_star path)")
+    ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "mxfp4"],
+                    help="FP4 format: nvfp4 (the method) or mxfp4 (Tab1a data-type ablation, NEXT #4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -222,7 +227,7 @@ def main():
     for i in range(H):
         Q[0, i], K[0, i], V[0, i] = synth.make_head(N, d, seed=0, b=0, h=rank * H + i, H=H * world,
                                                     dtype=torch.bfloat16, device=dev)
-    qkv = s3.FP4QKV(B, H, N, d, dev, smooth_q=args.smooth_q)
+    qkv = s3.FP4QKV(B, H, N, d, dev, smooth_q=args.smooth_q, fmt=args.fmt)
     O = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -295,13 +300,13 @@ def main():
                 "peak_source": f"{peak_src}: bf16_tflops {bf16_tf} x {FP4_OVER_BF16:g} (nominal dense FP4:BF16)",
                 "algorithmic": "4*B*H*N^2*d (x0.5 causal) per launch / mean CUDA-event launch time"}
     E = B * H * N * d
-    q_bytes = E * (3 * 2) + E * 3 * (0.5 + 1 / 16)  # read Q,K,V bf16; write codes + scales
+    q_bytes = E * (3 * 2) + E * 3 * (0.5 + (1 / 32 if args.fmt == "mxfp4" else 1 / 16))  # read bf16; write codes + scales
     quant = {"ms": q_ms, "algorithmic_bytes": q_bytes, "achieved_GBps": q_bytes / (q_ms * 1e-3) / 1e9,
              "peak_GBps": hbm_gbs, "frac": q_bytes / (q_ms * 1e-3) / 1e9 / hbm_gbs, "bound": "hbm"}
 
     # ---- e2e: the same step through the C-ABI host-buffer entry point (H2D + quantize + attn + D2H)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.fmt == "nvfp4":  # sage3_forward_host serves the method's format only
         qh, kh, vh = (x.cpu().pin_memory() for x in (Q, K, V))
         oh = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
         scratch = torch.empty(s3.sage3_forward_host_scratch_bytes(B, H, N, d), dtype=torch.uint8, device=dev)
@@ -334,7 +339,7 @@ def main():
         for n in (1024, 2048, 4096, 8192, 16384, 32768):
             for c in (False, True):
                 q2, k2, v2 = synth.make_qkv(1, H, n, d, seed=1, dtype=torch.bfloat16, device=dev)
-                f = s3.sage3_quantize_qkv(q2, k2, v2, stream=stream)
+                f = s3.sage3_quantize_qkv(q2, k2, v2, stream=stream, fmt=args.fmt)
                 o2 = torch.empty_like(q2)
                 reps = max(3, int(2e13 / attn_ops(1, H, n, d, c) / 50))
                 for _ in range(3):
@@ -364,7 +369,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": n_steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "nvfp4 (e2m1 codes, e4m3 1x16 scales), fp32 accumulate; bf16 in/out",
+            "dtype": ("nvfp4 (e2m1 codes, e4m3 1x16 scales)" if args.fmt == "nvfp4" else
+                      "mxfp4 (e2m1 codes, e8m0 1x32 scales)") + ", fp32 accumulate; bf16 in/out",
             "data": "synthetic (seeded Gaussian Q/K/V with outlier channels; synth/)",
             "config": cfg, "pct_fp4_peak": 100 * value / world / fp4_peak,
             "breakdown_ms": {"quantize": q_ms, "attention": a_ms},

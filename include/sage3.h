@@ -121,7 +121,7 @@ int sage3_kv_tile(int d);
  * Numerics (bit-exact with oracle_quantize_head): km[c] = fl32(Σ_chunks Σ_tokens K / N) in fp64 with the
  * fixed order of DESIGN.md reading c10; x = fl32(K - km); s = E4M3_RNE(fl32(amax·fl32(1/6)));
  * codes = E2M1_RNE(fl32(x·fl32(1/s))), all-zero codes when s == 0.  MXFP4 (out->fmt = SAGE3_MXFP4, Tab1a):
- * s = the smallest power of two >= fl32(amax·fl32(1/6)) (reading c11), code = E2M1_RNE(x / s) (exact
+ * s = the smallest power of two >= fl32(amax·fl32(1/6)) (reading m1), code = E2M1_RNE(x / s) (exact
  * scaling), scale byte 0 and zero codes when amax·fl32(1/6) == 0. */
 sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 v, sage3_dtype in_dtype, int B,
                                 int H, int N, int d, sage3_fp4_qkv* out, void* workspace, size_t workspace_bytes,

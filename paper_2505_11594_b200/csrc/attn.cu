@@ -220,7 +220,7 @@ __device__ unsigned long long g_trace[2][8][128][8];
 #endif
 
 // kSQ: smoothing Q (S += ds, Alg1 L8's GEMV term).  kMX: MXFP4 operands (Tab1a ablation): scale_vec::2X MMAs
-// with UE8M0 scales, P̂2 in 32-key blocks whose scale is the smallest power of two >= amax/6 (reading c11).
+// with UE8M0 scales, P̂2 in 32-key blocks whose scale is the smallest power of two >= amax/6 (reading m1).
 template <int D, bool kSQ, bool kMX>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,

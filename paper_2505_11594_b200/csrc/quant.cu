@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
           const float s32 = __fmul_rn(amax, kOneSixth);
           float rs;
           sc = e8m0_ceil(s32, rs);
-          const bool nz = real && s32 != 0.0f;  // amax = 0: scale byte 0 with zero codes (reading c11)
+          const bool nz = real && s32 != 0.0f;  // amax = 0: scale byte 0 with zero codes (reading m1)
           sc = nz ? sc : 0u;
           w = nz ? codes8(x, rs) : 0u;
         } else {

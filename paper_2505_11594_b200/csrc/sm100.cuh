@@ -289,7 +289,7 @@ __device__ __forceinline__ uint32_t cvt_e2m1x8(float a0, float a1, float a2, flo
   return r;
 }
 // packed e4m3x2 -> two halves (exact), used to decode a scale code.
-// MXFP4 scale (Tab1a ablation, reading c11): 2^p = the smallest power of two >= s32 (> 0, finite), p
+// MXFP4 scale (Tab1a ablation, reading m1): 2^p = the smallest power of two >= s32 (> 0, finite), p
 // clamped to [-127, 127] like the oracle; returns the UE8M0 code p + 127 and rs = 2^-p (x·rs = x / 2^p exactly).
 __device__ __forceinline__ uint32_t e8m0_ceil(float s32, float& rs) {
   const uint32_t b = __float_as_uint(s32), e = b >> 23, m = b & 0x7FFFFFu;

@@ -1,5 +1,5 @@
 """GPU parity of the MXFP4 data-type ablation (Tab1a; NEXT #4): the quantizer's E2M1 codes and
-UE8M0 scales (1x32 blocks, scale = smallest power of two >= amax/6, reading c11) BIT-EXACT against
+UE8M0 scales (1x32 blocks, scale = smallest power of two >= amax/6, reading m1) BIT-EXACT against
 oracle.quantize_head(fmt=FMT_MXFP4), and the scale_vec::2X attention path against the oracle's Algorithm 1 in
 the MXFP4 format on the same codes (north_star tolerance).  Also the data-type ordering the paper reports:
 NVFP4 more accurate than MXFP4, on the GPU path."""

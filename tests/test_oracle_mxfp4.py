@@ -43,7 +43,7 @@ def test_phi_mxfp4_against_its_definition():
 @pytest.mark.parametrize("causal", [False, True])
 def test_zero_scores_closed_form_mxfp4(causal):
     """Q = 0 => S = 0 => P̃ = 1, s_P1 = fl32(1/2688), P̃2 = 2688 -> E8M0 scale 512 (smallest 2^p >= 448),
-    code E2M1(5.25) = 6 -> deq 3072: O_i = mean_{j visible} deq(V̂)_j * 3072 * fl32(1/2688)."""
+    E2M1(5.25) = 6.0 (code 7) -> deq 3072: O_i = mean_{j visible} deq(V̂)_j * 3072 * fl32(1/2688)."""
     N, d = 300, 64
     _, K, V = (x.float().numpy() for x in synth.make_head(N, d, seed=2, dtype=torch.bfloat16))
     Q = np.zeros((N, d), np.float32)
