@@ -182,6 +182,8 @@ def workload_config(args, d):
         name += ",smooth-q"
     if getattr(args, "fmt", "nvfp4") != "nvfp4":
         name += "," + args.fmt
+    if getattr(args, "p_quant", "two_level") != "two_level":
+        name += ",p-" + args.p_quant
     return {"workload": name, "B": 1, "H": args.heads, "N": args.n, "d": d, "causal": bool(args.causal),
             "per_rank": True, "parallelism": f"heads-sharded x{args.gpus}",
             "l2": "inputs larger than L2 (3 x %.0f MB bf16 vs 126 MB)" % (args.heads * args.n * d * 2 / 1e6)}
@@ -202,6 +204,8 @@ def main():
     ap.add_argument("--smooth-q", action="store_true", help="Alg1 with smoothing Q (NEXT #1; off on the north_star path)")
     ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "mxfp4"],
                     help="FP4 format: nvfp4 (the method) or mxfp4 (Tab1a data-type ablation, NEXT #4)")
+    ap.add_argument("--p-quant", default="two_level", choices=["two_level", "direct"],
+                    help="P quantization: two_level (the method) or direct (Tab1b ablation, NEXT #4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -242,7 +246,7 @@ def main():
         if i is not None:
             ev_q[i][1].record(stream)
             ev_a[i][0].record(stream)
-        s3.sage3_attn_fwd(qkv, O, causal=causal, stream=stream)
+        s3.sage3_attn_fwd(qkv, O, causal=causal, stream=stream, p_quant=args.p_quant)
         if i is not None:
             ev_a[i][1].record(stream)
 
@@ -306,7 +310,7 @@ def main():
 
     # ---- e2e: the same step through the C-ABI host-buffer entry point (H2D + quantize + attn + D2H)
     e2e = None
-    if not args.no_e2e and args.fmt == "nvfp4":  # sage3_forward_host serves the method's format only
+    if not args.no_e2e and args.fmt == "nvfp4" and args.p_quant == "two_level":  # (the method's path only)
         qh, kh, vh = (x.cpu().pin_memory() for x in (Q, K, V))
         oh = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
         scratch = torch.empty(s3.sage3_forward_host_scratch_bytes(B, H, N, d), dtype=torch.uint8, device=dev)
@@ -343,11 +347,11 @@ def main():
                 o2 = torch.empty_like(q2)
                 reps = max(3, int(2e13 / attn_ops(1, H, n, d, c) / 50))
                 for _ in range(3):
-                    s3.sage3_attn_fwd(f, o2, causal=c, stream=stream)
+                    s3.sage3_attn_fwd(f, o2, causal=c, stream=stream, p_quant=args.p_quant)
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
                 for _ in range(reps):
-                    s3.sage3_attn_fwd(f, o2, causal=c, stream=stream)
+                    s3.sage3_attn_fwd(f, o2, causal=c, stream=stream, p_quant=args.p_quant)
                 a1.record(stream)
                 torch.cuda.synchronize()
                 ms = a0.elapsed_time(a1) / reps

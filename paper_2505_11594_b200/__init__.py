@@ -20,12 +20,14 @@ SAGE3_OK, SAGE3_ERR_INVALID_ARG, SAGE3_ERR_UNSUPPORTED, SAGE3_ERR_WORKSPACE, SAG
 SAGE3_FP16, SAGE3_BF16, SAGE3_FP32 = 0, 1, 2
 SAGE3_NVFP4, SAGE3_MXFP4 = 0, 1  # sage3_fp4_format: the method / the Tab1a data-type ablation
 _FMT = {"nvfp4": SAGE3_NVFP4, "mxfp4": SAGE3_MXFP4, SAGE3_NVFP4: SAGE3_NVFP4, SAGE3_MXFP4: SAGE3_MXFP4}
+SAGE3_P_TWO_LEVEL, SAGE3_P_DIRECT = 0, 1  # sage3_p_quant: the method / the Tab1b ablation
+_PQ = {"two_level": SAGE3_P_TWO_LEVEL, "direct": SAGE3_P_DIRECT}
 _DT = {torch.float16: SAGE3_FP16, torch.bfloat16: SAGE3_BF16, torch.float32: SAGE3_FP32}
 
 # Every function include/sage3.h declares (checked by tests/test_abi.py).
 ABI_FUNCTIONS = (
     "sage3_fp4_qkv_sizes", "sage3_fp4_qkv_sizes_fmt", "sage3_smooth_q_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
-    "sage3_attn_fwd", "sage3_attn_fwd_units", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
+    "sage3_attn_fwd", "sage3_attn_fwd_units", "sage3_attn_fwd_ex", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
     "sage3_last_cuda_error", "sage3_version",
 )
 
@@ -43,6 +45,11 @@ class FP4QKVStruct(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("N", ctypes.c_int32), ("d", ctypes.c_int32),
                 ("N_pad", ctypes.c_int32), ("fmt", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in (
                     "q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean", "q_mean", "ds")]
+
+
+class AttnOptions(ctypes.Structure):
+    _fields_ = [("causal", ctypes.c_int32), ("softmax_scale", ctypes.c_float), ("p_quant", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("unit_begin", ctypes.c_int64), ("unit_end", ctypes.c_int64)]
 
 
 _lib = None
@@ -72,6 +79,8 @@ def load() -> ctypes.CDLL:
     L.sage3_attn_fwd_units.argtypes = [ctypes.POINTER(FP4QKVStruct), Tensor4, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_float, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                        ctypes.c_void_p]
+    L.sage3_attn_fwd_ex.argtypes = [ctypes.POINTER(FP4QKVStruct), Tensor4, ctypes.c_int,
+                                    ctypes.POINTER(AttnOptions), ctypes.c_void_p, ctypes.c_void_p]
     L.sage3_forward_host_scratch_bytes.argtypes = [ctypes.c_int] * 6
     L.sage3_forward_host_scratch_bytes.restype = sz
     L.sage3_forward_host.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 6 + [ctypes.c_float, ctypes.c_void_p,
@@ -184,14 +193,32 @@ def sage3_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: F
 
 def sage3_attn_fwd(qkv: FP4QKV, o: torch.Tensor | None = None, *, causal: bool = False,
                    softmax_scale: float = 0.0, lse: torch.Tensor | None = None, out_dtype=torch.bfloat16,
-                   stream=None) -> torch.Tensor:
-    """Alg1 L6-L13 (FP4 QK^T, online softmax, two-level P, FP4 PV, O/l): see include/sage3.h."""
+                   stream=None, p_quant: str = "two_level") -> torch.Tensor:
+    """Alg1 L6-L13 (FP4 QK^T, online softmax, two-level P, FP4 PV, O/l): see include/sage3.h.
+    p_quant="direct" selects the Tab1b ablation (sage3_attn_fwd_ex)."""
     if o is None:
         o = torch.empty(qkv.B, qkv.H, qkv.N, qkv.d, dtype=out_dtype, device=qkv.q_data.device)
+    if p_quant != "two_level":
+        return sage3_attn_fwd_ex(qkv, o, causal=causal, softmax_scale=softmax_scale, lse=lse, stream=stream,
+                                 p_quant=p_quant)
     lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
     st = load().sage3_attn_fwd(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], 1 if causal else 0,
                                float(softmax_scale), lse_p, _stream(stream))
     _check(st, "sage3_attn_fwd")
+    return o
+
+
+def sage3_attn_fwd_ex(qkv: FP4QKV, o: torch.Tensor, *, causal: bool = False, softmax_scale: float = 0.0,
+                      lse: torch.Tensor | None = None, stream=None, p_quant: str = "two_level", unit_begin: int = 0,
+                      unit_end: int = -1) -> torch.Tensor:
+    """sage3_attn_fwd_ex: the attention with a sage3_attn_options struct (P quantization mode, unit range)."""
+    if p_quant not in _PQ:
+        raise Sage3Error(f"unknown p_quant {p_quant!r}")
+    opts = AttnOptions(1 if causal else 0, float(softmax_scale), _PQ[p_quant], 0, int(unit_begin), int(unit_end))
+    lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
+    st = load().sage3_attn_fwd_ex(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], ctypes.byref(opts), lse_p,
+                                  _stream(stream))
+    _check(st, "sage3_attn_fwd_ex")
     return o
 
 
@@ -231,11 +258,11 @@ def sage3_forward_host(q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
               softmax_scale: float = 0.0, out_dtype=None, stream=None, smooth_q: bool = False,
-              fmt="nvfp4") -> torch.Tensor:
+              fmt="nvfp4", p_quant: str = "two_level") -> torch.Tensor:
     """Quantize + attention in one call (the two ABI calls, enqueued on the current stream)."""
     qkv = sage3_quantize_qkv(q, k, v, stream=stream, smooth_q=smooth_q, fmt=fmt)
     return sage3_attn_fwd(qkv, causal=causal, softmax_scale=softmax_scale, out_dtype=out_dtype or q.dtype,
-                          stream=stream)
+                          stream=stream, p_quant=p_quant)
 
 
 def default_scale(d: int) -> float:

@@ -156,13 +156,19 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
 }
 
-sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
-                                  float softmax_scale, float* lse, int64_t unit_begin, int64_t unit_end,
-                                  void* stream) {
-  if (!qkv || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
+sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype,
+                               const sage3_attn_options* opts, float* lse, void* stream) {
+  if (!qkv || !opts || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
+  if ((opts->p_quant != SAGE3_P_TWO_LEVEL && opts->p_quant != SAGE3_P_DIRECT) || opts->reserved != 0)
+    return SAGE3_ERR_INVALID_ARG;
+  if (opts->p_quant == SAGE3_P_DIRECT && (qkv->q_mean || qkv->ds)) return SAGE3_ERR_INVALID_ARG;
+  const int causal = opts->causal;
+  const float softmax_scale = opts->softmax_scale;
+  const int64_t unit_begin = opts->unit_begin;
   if (qkv->N_pad != npad(qkv->N)) return SAGE3_ERR_INVALID_ARG;
   if (qkv->fmt != SAGE3_NVFP4 && qkv->fmt != SAGE3_MXFP4) return SAGE3_ERR_INVALID_ARG;
   const int64_t n_units = (int64_t)qkv->B * qkv->H * (qkv->N_pad / 128);
+  const int64_t unit_end = opts->unit_end < 0 ? n_units : opts->unit_end;
   if (unit_begin < 0 || unit_end < unit_begin || unit_end > n_units || unit_end - unit_begin > 0x7FFFFFFF)
     return SAGE3_ERR_INVALID_ARG;
   if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
@@ -180,6 +186,7 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
   sage3::AttnArgs a{};
   a.ds = qkv->ds;
   a.mx = qkv->fmt == SAGE3_MXFP4;
+  a.p_direct = opts->p_quant == SAGE3_P_DIRECT;
   a.q_data = qkv->q_data, a.k_data = qkv->k_data, a.v_data = qkv->v_data;
   a.q_sf = qkv->q_sf, a.k_sf = qkv->k_sf, a.v_sf = qkv->v_sf;
   a.o = o.ptr, a.o_sb = o.stride_b, a.o_sh = o.stride_h, a.o_sn = o.stride_n, a.o_dtype = (int)o_dtype;
@@ -190,6 +197,16 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
   a.unit_begin = unit_begin, a.unit_end = unit_end;
   cudaError_t e = sage3::launch_attention(a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
+}
+
+sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                                  float softmax_scale, float* lse, int64_t unit_begin, int64_t unit_end,
+                                  void* stream) {
+  if (unit_end < 0) return SAGE3_ERR_INVALID_ARG;  // (the options' "to the end" value is not part of this API)
+  sage3_attn_options op{};
+  op.causal = causal, op.softmax_scale = softmax_scale, op.p_quant = SAGE3_P_TWO_LEVEL;
+  op.unit_begin = unit_begin, op.unit_end = unit_end;
+  return sage3_attn_fwd_ex(qkv, o, o_dtype, &op, lse, stream);
 }
 
 sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,

@@ -102,7 +102,8 @@ struct Layout {
   static constexpr int oXchg = oPSF + kPBufs * kPSF;            // float [kXSlots][2][128]: tmax_j, rowsum(P̃2_j)
   static constexpr int oDs = oXchg + kXSlots * 2 * 128 * 4;  // smoothing Q: ds rows of 128 keys, kDsStages slots
   static constexpr int oBar = oDs + kDsStages * 512;
-  static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + kXSlots + 2 * kDsStages;
+  static constexpr int kNumBars =
+      1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
@@ -221,7 +222,11 @@ __device__ unsigned long long g_trace[2][8][128][8];
 
 // kSQ: smoothing Q (S += ds, Alg1 L8's GEMV term).  kMX: MXFP4 operands (Tab1a ablation): scale_vec::2X MMAs
 // with UE8M0 scales, P̂2 in 32-key blocks whose scale is the smallest power of two >= amax/6 (reading m1).
-template <int D, bool kSQ, bool kMX>
+// kDirect: the direct-P ablation (Tab1b): P̂ = φ(P̃) with P̃ = exp(scale(S - m_j)) relative to the
+// RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
+// of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
+// warpgroups are no longer independent in this mode.
+template <int D, bool kSQ, bool kMX, bool kDirect>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const AttnArgs a) {
@@ -247,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8
   uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (TMA)
   uint64_t* ds_empty = ds_full + kDsStages;  // softmax -> V producer: slot read
+  uint64_t* m_full = ds_empty + kDsStages;    // direct P: m_j of tile j in xchg slot j%8 (softmax -> softmax)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -279,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_empty[b], 1);
     }
     for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], kXArrivals);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&m_full[s], 128);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
       mbar_init(&ds_empty[s], 4);  // one arrival per softmax warp of the tile's warpgroup
@@ -503,7 +510,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
-      const float nb = kLog2_2688 - tmax * sl2;  // P̃2 = 2^(S·sl2 + nb)
+      const int slot = j % kXSlots;
+      // the exponent reference of this tile's values: tmax_j (two-level: P̃2 = 2688·2^{sl2(S - tmax_j)}) or the
+      // running max m_j (direct: P̃ = 2^{sl2(S - m_j)}); the correction warpgroup weights the tile by it
+      float eref = tmax;
+      if constexpr (kDirect) {
+        float mp = -INFINITY;
+        if (j > 0) {
+          const int ps = (j - 1) % kXSlots;
+          mbar_wait(&m_full[ps], (uint32_t)((j - 1) / kXSlots) & 1u);
+          mp = lds_f32(xchg_s + ps * 1024);
+        }
+        eref = fmaxf(mp, tmax);
+        sts_f32(xchg_s + slot * 1024, eref);
+        mbar_arrive(&m_full[slot]);  // per thread: orders its own slot write
+      }
+      const float nb = kDirect ? -eref * sl2 : kLog2_2688 - tmax * sl2;  // P̃2 (P̃) = 2^(S·sl2 + nb)
       if constexpr (masked || kSQ) tmem_st_wait();
       uint32_t va[32], vb[32];
       tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
@@ -606,8 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       sts_u32(sPSF, scw[0]);
       if constexpr (!kMX) sts_u32(sPSF + 512, scw[1]);
-      const int slot = j % kXSlots;
-      sts_f32(xchg_s + slot * 1024, tmax);
+      if constexpr (!kDirect) sts_f32(xchg_s + slot * 1024, eref);
       sts_f32(xchg_s + slot * 1024 + 512, rowsum);
       tc_fence_before();
       fence_proxy_async_smem();
@@ -664,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], sc2);
         mref = mnew;
       }
-      const float w = ex2((tmax - mref) * sl2 - kLog2_2688);
+      const float w = ex2((tmax - mref) * sl2 - (kDirect ? 0.0f : kLog2_2688));  // tmax = the tile's eref
       l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
       mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
@@ -758,14 +779,14 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, bool kSQ, bool kMX>
+template <int D, bool kSQ, bool kMX, bool kDirect>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
   using L = Layout<D, kMX>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
@@ -777,7 +798,7 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_fwd_kernel<D, kSQ, kMX><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
+  attn_fwd_kernel<D, kSQ, kMX, kDirect><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
   return cudaGetLastError();
 }
 
@@ -785,8 +806,11 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
 
 template <bool kMX>
 cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
-  if (a.ds) return a.d == 128 ? launch_d<128, true, kMX>(a, stream) : launch_d<64, true, kMX>(a, stream);
-  return a.d == 128 ? launch_d<128, false, kMX>(a, stream) : launch_d<64, false, kMX>(a, stream);
+  if (a.p_direct) {  // ablation: no smoothing-Q instantiation (rejected in abi.cu)
+    return a.d == 128 ? launch_d<128, false, kMX, true>(a, stream) : launch_d<64, false, kMX, true>(a, stream);
+  }
+  if (a.ds) return a.d == 128 ? launch_d<128, true, kMX, false>(a, stream) : launch_d<64, true, kMX, false>(a, stream);
+  return a.d == 128 ? launch_d<128, false, kMX, false>(a, stream) : launch_d<64, false, kMX, false>(a, stream);
 }
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream) {

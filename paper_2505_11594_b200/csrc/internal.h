@@ -42,6 +42,7 @@ struct AttnArgs {
   float scale;  // softmax scale (S units)
   const float* ds;  // smoothing Q (nullable): [B][H][Np/128][Np], added to S
   bool mx;          // MXFP4 operands (scale_vec::2X MMAs, 32-key P̂2 blocks with E8M0 scales)
+  bool p_direct;    // direct-P ablation (Tab1b): P̂ = φ(P̃) relative to the running max, s_P1 = 1
   int64_t unit_begin, unit_end;  // work units [begin, end) of the flattened (b·h, q-tile) space
 };
 

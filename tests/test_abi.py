@@ -71,6 +71,10 @@ def test_invalid_arguments_rejected_before_any_cuda_call(lib):
     t = s3.Tensor4(16, 0, 0, 64)  # misaligned-free fake pointer, but the qkv buffers are null
     st = lib.sage3_attn_fwd(ctypes.byref(f), t, s3.SAGE3_BF16, 0, 0.0, None, None)
     assert st == s3.SAGE3_ERR_INVALID_ARG
+    for opts in (None, s3.AttnOptions(0, 0.0, 2, 0, 0, -1), s3.AttnOptions(0, 0.0, 0, 1, 0, -1)):
+        st = lib.sage3_attn_fwd_ex(ctypes.byref(f), t, s3.SAGE3_BF16, ctypes.byref(opts) if opts else None, None,
+                                   None)
+        assert st == s3.SAGE3_ERR_INVALID_ARG  # null options, unknown p_quant, non-zero reserved
     f.fmt = 7  # not a sage3_fp4_format
     st = lib.sage3_quantize_qkv(t, t, t, s3.SAGE3_BF16, 1, 1, 128, 64, ctypes.byref(f), None, 0, None, None)
     assert st == s3.SAGE3_ERR_INVALID_ARG

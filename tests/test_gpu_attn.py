@@ -24,7 +24,7 @@ def oracle_heads(qkv, heads):
     out = []
     for bh in heads:
         g = decode_head(qkv, bh)
-        h = oracle.QuantizedHead(qkv.N, qkv.d)
+        h = oracle.QuantizedHead(qkv.N, qkv.d, fmt=qkv.fmt)  # the library's sage3_fp4_format = oracle FMT_*
         h.q_codes, h.k_codes, h.v_codes = g["q_codes"], g["k_codes"], g["v_codes"]
         h.q_sf, h.k_sf, h.v_sf = g["q_sf"], g["k_sf"], np.ascontiguousarray(g["v_sf_full"][: qkv.d])
         out.append(h)
@@ -277,3 +277,51 @@ def test_abi_rejects_bad_unit_ranges_and_half_smooth_q():
     qkv.struct.q_mean = qkv.k_mean.data_ptr()  # q_mean without ds
     with pytest.raises(s3.Sage3Error):
         s3.sage3_attn_fwd(qkv, o)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "mxfp4"])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("N,d", [(128, 128), (300, 64), (1024, 128)])
+def test_direct_p_ablation_parity(N, d, causal, fmt):
+    """Tab1b's direct-P ablation on the GPU (sage3_attn_fwd_ex, p_quant = direct): P̂ = φ(P̃) relative to the
+    running max, s_P1 = 1, against the oracle's PMODE_DIRECT on the same codes, north_star tolerance."""
+    B, H = 1, 2
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=13 * N + d, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V, fmt=fmt)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device="cuda")
+    O = s3.sage3_attn_fwd(qkv, causal=causal, out_dtype=torch.float32, lse=lse, p_quant="direct")
+    torch.cuda.synchronize()
+    heads = oracle_heads(qkv, range(B * H))
+    ref, ref_lse = oracle.attn_fwd(heads, causal=causal, scale=1 / math.sqrt(d), p_mode=oracle.PMODE_DIRECT,
+                                   want_lse=True)
+    for bh in range(B * H):
+        check(O[0, bh].cpu().numpy(), ref[bh], torch.float32, f"head {bh}")
+    np.testing.assert_allclose(lse.cpu().numpy().reshape(B * H, N), ref_lse, rtol=1e-5, atol=1e-4)
+    # the unit-range form of the same call is bitwise identical
+    O2 = torch.zeros_like(O)
+    n = s3.n_units(qkv)
+    s3.sage3_attn_fwd_ex(qkv, O2, causal=causal, p_quant="direct", unit_begin=0, unit_end=n // 2)
+    s3.sage3_attn_fwd_ex(qkv, O2, causal=causal, p_quant="direct", unit_begin=n // 2)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O2)
+
+
+def test_two_level_beats_direct_p_on_gpu():
+    """Tab1b: two-level P quantization is more accurate than direct φ(P̃) (the E4M3 scales of
+    P̃ <= 1 underflow), measured on the GPU path against fp64 attention."""
+    N, d = 4096, 128
+    Q, K, V = synth.make_qkv(1, 1, N, d, seed=41, dtype=torch.bfloat16, device="cuda")
+    rows = np.arange(0, N, 16, dtype=np.int32)
+    ref = oracle.reference_attention(Q[0, 0].float().cpu().numpy(), K[0, 0].float().cpu().numpy(),
+                                     V[0, 0].float().cpu().numpy(), causal=False, scale=1 / math.sqrt(d), rows=rows)
+    m = {p: oracle.accuracy_metrics(ref, s3.attention(Q, K, V, p_quant=p, out_dtype=torch.float32)[0, 0].cpu().numpy()[rows])
+         for p in ("two_level", "direct")}
+    print("GPU two-level / direct P:", m)
+    assert m["two_level"]["cos_sim"] > m["direct"]["cos_sim"] and m["two_level"]["l1"] < m["direct"]["l1"]
+
+
+def test_direct_p_rejects_smoothing_q():
+    Q, K, V = synth.make_qkv(1, 1, 256, 64, seed=2, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V, smooth_q=True)
+    with pytest.raises(s3.Sage3Error):
+        s3.sage3_attn_fwd(qkv, p_quant="direct")
