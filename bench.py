@@ -204,8 +204,8 @@ def main():
     ap.add_argument("--smooth-q", action="store_true", help="Alg1 with smoothing Q (NEXT #1; off on the north_star path)")
     ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "mxfp4"],
                     help="FP4 format: nvfp4 (the method) or mxfp4 (Tab1a data-type ablation, NEXT #4)")
-    ap.add_argument("--p-quant", default="two_level", choices=["two_level", "direct"],
-                    help="P quantization: two_level (the method) or direct (Tab1b ablation, NEXT #4)")
+    ap.add_argument("--p-quant", default="two_level", choices=["two_level", "direct", "lazy"],
+                    help="P quantization: two_level (the method), direct (Tab1b ablation, NEXT #4), lazy (NEXT #2 variant)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

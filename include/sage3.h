@@ -151,12 +151,15 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
 /* Options of sage3_attn_fwd_ex (zero-initialise, then set what differs from the defaults). */
 typedef enum {
   SAGE3_P_TWO_LEVEL = 0, /* the method: s_P1 = rowmax(P̃)/(448·6), P̂2 = φ(P̃/s_P1) (§3.2, Alg1 L10)   */
-  SAGE3_P_DIRECT = 1     /* ablation (Tab1b): P̂ = φ(P̃), P̃ = exp(scale(S - m_j)) with the running max */
+  SAGE3_P_DIRECT = 1,    /* ablation (Tab1b): P̂ = φ(P̃), P̃ = exp(scale(S - m_j)) with the running max */
+  SAGE3_P_TWO_LEVEL_LAZY = 2 /* throughput variant (reading n1): the first level
+                              * is a per-row reference r moved to the tile max only when that exceeds r by more
+                              * than 2^8 in weight; P̂2 = φ(10.5·exp(scale(S - r))); O accumulates in TMEM      */
 } sage3_p_quant;
 typedef struct {
   int32_t causal;       /* != 0: key j visible to query i iff j <= i                                      */
   float softmax_scale;  /* <= 0 selects 1/sqrt(d)                                                          */
-  int32_t p_quant;      /* sage3_p_quant; SAGE3_P_DIRECT requires smoothing Q off (else INVALID_ARG)        */
+  int32_t p_quant;      /* sage3_p_quant; modes other than TWO_LEVEL require smoothing Q off (INVALID_ARG)  */
   int32_t reserved;     /* must be 0                                                                       */
   int64_t unit_begin;   /* work units [unit_begin, unit_end) as in sage3_attn_fwd_units;                   */
   int64_t unit_end;     /*   unit_end < 0 selects every unit from unit_begin on                            */
@@ -164,9 +167,11 @@ typedef struct {
 
 /* sage3_attn_fwd_units with an options struct (the other two entry points are this call with p_quant =
  * SAGE3_P_TWO_LEVEL).  The direct-P mode chains the running max through the KV tiles (the two softmax
- * warpgroups of the kernel wait on each other) and is an accuracy ablation, not a fast path.
+ * warpgroups of the kernel wait on each other) and is an accuracy ablation, not a fast path.  The lazy mode
+ * runs a second kernel (O accumulated by the tensor core in TMEM, S rows kept in registers) whose results
+ * match the oracle's PMODE_LAZY, not Alg1 L10; lse = scale·r + ln(l / 10.5) is the same quantity.
  * Errors: as sage3_attn_fwd_units; SAGE3_ERR_INVALID_ARG also for opts == NULL, an unknown p_quant, a
- * non-zero reserved field, or SAGE3_P_DIRECT with smoothing Q. */
+ * non-zero reserved field, or a mode other than SAGE3_P_TWO_LEVEL with smoothing Q. */
 sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype,
                                const sage3_attn_options* opts, float* lse, void* stream);
 

@@ -29,7 +29,7 @@ _CFLAGS = ["-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fopenmp",
 _lock = threading.Lock()
 _lib = None
 
-PMODE_TWO_LEVEL, PMODE_DIRECT, PMODE_NONE = 0, 1, 2
+PMODE_TWO_LEVEL, PMODE_DIRECT, PMODE_NONE, PMODE_LAZY = 0, 1, 2, 3  # LAZY: NEXT #2 variant (reading n1)
 
 
 def build(force: bool = False) -> str:

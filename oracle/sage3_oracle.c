@@ -18,6 +18,8 @@
  *   Alg1 L10   s_P1 = rowmax(P̃)/(448*6), P̃2 = P̃/s_P1, (s_P2, P̂2) = φ(P̃2)   (§3.2)
  *   Alg1 L11   O = diag(e^{m_old-m}) O + FP4MM(P̂2, s_P2, V̂, s_V) * s_P1
  *   Alg1 L13   O = diag(l)^-1 O
+ *   (variant)  p_mode LAZY: the first-level P scale per row per reference epoch instead of per tile
+ *              (reading n1)            -> attn_row_lazy
  * Precision: every quantizer is bit-exact fp32 arithmetic; P̃, P̃2 and s_P1 are fp32 as P:188 states;
  * everything else is fp64.  The readings of points the paper leaves open (rounding modes, the 1/6
  * multiply, softmax scale, causal mask, padding, s_P1 granularity) are SURVEY.md §8(c) c1-c16 and are
@@ -325,6 +327,7 @@ EXPORT void oracle_fp4mm(const uint8_t* a_codes, const uint8_t* a_sf, const uint
 #define PMODE_TWO_LEVEL 0
 #define PMODE_DIRECT 1
 #define PMODE_NONE 2
+#define PMODE_LAZY 3 /* NEXT #2 throughput variant (not the paper's Alg1 L10): see attn_row_lazy */
 
 EXPORT float oracle_two_level_row_fmt(const float* P, int n, int p_mode, int fmt, uint8_t* codes, uint8_t* sf) {
   const int G = fmt ? 32 : 16;
@@ -357,6 +360,83 @@ EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* co
 }
 
 /* ------------------------------------------------------------------------------------------------
+ * NEXT #2 variant (reading n1; NOT the paper's Alg1 L10): two-level P whose first level is a
+ * lazily moved per-row reference r instead of each tile's own row max.  Per KV tile j, after S (Alg1 L8):
+ *   if r = -inf or log2(e)·scale·(tmax_j - r) > LAZY_TAU:  O *= exp(scale(r - tmax_j)), l *= the same,
+ *                                                          r = tmax_j        (the reference moves up)
+ *   P̃2 = fl32(LAZY_TOP · exp(scale(S - r)))    LAZY_TOP = 2688 / 2^LAZY_TAU = 10.5, so P̃2 <= 2688 always
+ *                                               (tmax_j <= r + LAZY_TAU / (log2(e)·scale))
+ *   l += Σ P̃2 (unquantized, as reading c9);  (s_P2, P̂2) = φ(P̃2) per 16 (or 32, MXFP4) keys (Alg1 L10's
+ *   second level);  O += FP4MM(P̂2, s_P2, V̂, s_V)   (no per-tile first-level factor)
+ * and O/l at the end; lse = scale·r + ln(l / LAZY_TOP).  O/l equals Alg1's up to quantization: every tile of
+ * an epoch shares the scale 2^-LAZY_TAU·2688·exp(scale(m - r)) relative to P̃, so the tensor core can
+ * accumulate O across tiles (the GPU keeps O in TMEM) and only a moving reference costs a rescale.
+ * ------------------------------------------------------------------------------------------------ */
+#define LAZY_TAU 8.0
+#define LAZY_TOP 10.5 /* 2688 * 2^-8, exact */
+static void attn_row_lazy(const double* Qrow, const double* Kd, const double* Vt, int N, int Np, int d, int Bkv,
+                          int causal, int qi, double scale, const float* qbar, const float* Ks, int fmt, double* O,
+                          double* lse) {
+  const int G = fmt ? 32 : 16;
+  double r = -INFINITY, l = 0.0;
+  double* S = (double*)malloc(sizeof(double) * (size_t)Bkv);
+  float* P2 = (float*)malloc(sizeof(float) * (size_t)Bkv);
+  uint8_t* pc = (uint8_t*)malloc((size_t)Bkv);
+  uint8_t* ps = (uint8_t*)malloc((size_t)Bkv / 16 + 1);
+  for (int c = 0; c < d; ++c) O[c] = 0.0;
+  int kv_end = causal ? (qi + 1 < N ? qi + 1 : N) : N;
+  for (int j0 = 0; j0 < kv_end; j0 += Bkv) {
+    double tmax = -INFINITY;
+    for (int t = 0; t < Bkv; ++t) { /* Alg1 L8, exactly as attn_row */
+      int key = j0 + t;
+      if (key >= kv_end || key >= Np) {
+        S[t] = -INFINITY;
+        continue;
+      }
+      double acc = 0.0;
+      for (int c = 0; c < d; ++c) acc += Qrow[c] * Kd[(size_t)key * d + c];
+      if (qbar) {
+        double g = 0.0;
+        for (int c = 0; c < d; ++c) g += (double)qbar[c] * (double)Ks[(size_t)key * d + c];
+        acc += g;
+      }
+      S[t] = acc;
+      if (acc > tmax) tmax = acc;
+    }
+    if (r == -INFINITY || (tmax - r) * scale / log(2.0) > LAZY_TAU) { /* move the reference */
+      double a = (r == -INFINITY) ? 0.0 : exp(scale * (r - tmax));
+      for (int c = 0; c < d; ++c) O[c] *= a;
+      l *= a;
+      r = tmax;
+    }
+    for (int t = 0; t < Bkv; ++t) {
+      P2[t] = (S[t] == -INFINITY) ? 0.0f : (float)(LAZY_TOP * exp(scale * (S[t] - r)));
+      l += (double)P2[t];
+    }
+    for (int b = 0; b < Bkv; b += G) {
+      if (fmt) oracle_phi_mxfp4(&P2[b], &pc[b], &ps[b / G]);
+      else oracle_phi_nvfp4(&P2[b], &pc[b], &ps[b / G]);
+    }
+    for (int c = 0; c < d; ++c) {
+      double pv = 0.0;
+      for (int t = 0; t < Bkv; ++t) {
+        int key = j0 + t;
+        if (key >= Np) break;
+        double p = oracle_e2m1_decode(pc[t]) * (fmt ? ldexp(1.0, (int)ps[t / 32] - 127) : oracle_e4m3_decode(ps[t / 16]));
+        pv += p * Vt[(size_t)c * Np + key];
+      }
+      O[c] += pv;
+    }
+  }
+  for (int c = 0; c < d; ++c) O[c] /= l;
+  if (lse) *lse = scale * r + log(l / LAZY_TOP);
+  free(S);
+  free(P2);
+  free(pc);
+  free(ps);
+}
+
+/* ------------------------------------------------------------------------------------------------
  * (3) Attention for ONE query row of one head: Alg1 L6-L13 with the online softmax of FlashAttention
  * (P:71), tiled over keys in blocks of Bkv.  Operands are given dequantized (exact, fp64):
  *   Qrow [d], Kd [Np][d], Vt [d][Np] (V transposed), codes only matter through these values.
@@ -370,6 +450,10 @@ EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* co
 static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int N, int Np, int d, int Bkv,
                      int causal, int qi, double scale, int p_mode, const float* qbar, const float* Ks, int fmt,
                      double* O, double* lse) {
+  if (p_mode == PMODE_LAZY) {
+    attn_row_lazy(Qrow, Kd, Vt, N, Np, d, Bkv, causal, qi, scale, qbar, Ks, fmt, O, lse);
+    return;
+  }
   double m = -INFINITY, l = 0.0;
   double* S = (double*)malloc(sizeof(double) * (size_t)Bkv);
   float* Pt = (float*)malloc(sizeof(float) * (size_t)Bkv);

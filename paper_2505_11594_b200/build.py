@@ -12,8 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsage3.so")
-SOURCES = ["abi.cu", "quant.cu", "attn.cu"]
-HEADERS = ["sm100.cuh", "internal.h", os.path.join("..", "..", "include", "sage3.h")]
+SOURCES = ["abi.cu", "quant.cu", "attn.cu", "attn_lazy.cu"]
+HEADERS = ["sm100.cuh", "attn_common.cuh", "internal.h", os.path.join("..", "..", "include", "sage3.h")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",

@@ -159,9 +159,11 @@ sage3_status sage3_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 
 sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype,
                                const sage3_attn_options* opts, float* lse, void* stream) {
   if (!qkv || !opts || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
-  if ((opts->p_quant != SAGE3_P_TWO_LEVEL && opts->p_quant != SAGE3_P_DIRECT) || opts->reserved != 0)
+  if ((opts->p_quant != SAGE3_P_TWO_LEVEL && opts->p_quant != SAGE3_P_DIRECT &&
+       opts->p_quant != SAGE3_P_TWO_LEVEL_LAZY) ||
+      opts->reserved != 0)
     return SAGE3_ERR_INVALID_ARG;
-  if (opts->p_quant == SAGE3_P_DIRECT && (qkv->q_mean || qkv->ds)) return SAGE3_ERR_INVALID_ARG;
+  if (opts->p_quant != SAGE3_P_TWO_LEVEL && (qkv->q_mean || qkv->ds)) return SAGE3_ERR_INVALID_ARG;
   const int causal = opts->causal;
   const float softmax_scale = opts->softmax_scale;
   const int64_t unit_begin = opts->unit_begin;
@@ -195,7 +197,9 @@ sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_
   a.causal = causal ? 1 : 0;
   a.scale = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)qkv->d);
   a.unit_begin = unit_begin, a.unit_end = unit_end;
-  cudaError_t e = sage3::launch_attention(a, static_cast<cudaStream_t>(stream));
+  cudaError_t e = opts->p_quant == SAGE3_P_TWO_LEVEL_LAZY
+                      ? sage3::launch_attention_lazy(a, static_cast<cudaStream_t>(stream))
+                      : sage3::launch_attention(a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
 }
 

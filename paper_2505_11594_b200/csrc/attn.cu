@@ -34,6 +34,7 @@
 #include <mutex>
 #include <type_traits>
 
+#include "attn_common.cuh"
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -50,14 +51,6 @@ constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j
 #endif
 constexpr int kXArrivals = SAGE3_X_ARRIVALS;  // x_full arrivals per tile: 128 (per thread) or 4 (per warp)
 constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
-#ifndef SAGE3_POLY_MASK
-#define SAGE3_POLY_MASK 0x1111
-#endif
-#ifndef SAGE3_POLY_DEGREE
-#define SAGE3_POLY_DEGREE 4
-#endif
-// bit i set: exp2 pair i of each 32-key chunk (16 pairs) runs on the FMA pipe (polynomial), else on MUFU
-constexpr uint32_t kPolyMask = SAGE3_POLY_MASK;
 constexpr int kThreads = 512;
 // Per-thread register budgets after setmaxnreg (one warp of each warpgroup per SM sub-partition:
 // kRegWG0 + 2 kRegSoftmax + kRegCorrection = 512 = 64K registers / 128 lanes).
@@ -68,15 +61,11 @@ constexpr int kThreads = 512;
 #endif
 constexpr uint32_t kRegWG0 = SAGE3_REG_WG0, kRegSoftmax = SAGE3_REG_SOFTMAX, kRegCorrection = SAGE3_REG_CORRECTION;
 static_assert(kRegWG0 + 2 * kRegSoftmax + kRegCorrection <= 512, "register budget");
-constexpr float kOneSixth = 0x1.555556p-3f;  // fl32(1/6)
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLog2_2688 = 11.392317422778761f;  // log2(448 * 6)
 
 // TMEM column map (512 columns allocated): three 128-column buffers; tile j uses buffer j % 3 first for
 // S_j (MMA), then — once the softmax has read S_j — for PV_j (MMA), which the correction warpgroup reads
 // before the buffer is reused for S_{j+3}.  Scale factors in 32 more columns.
 constexpr int kSBufs = 3;
-constexpr uint32_t kColSFQ = 384, kColSFK = 392, kColSFV = 400, kColSFP = 408;
 
 template <int D, bool kMX>
 struct Layout {
@@ -109,116 +98,6 @@ struct Layout {
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
 };
 
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// 2^x for a pair on the FMA pipe (offloads MUFU): x = j + f with j = rint(x), f in [-0.5, 0.5];
-// 2^f by a degree-5 fp32 minimax polynomial (max rel. error 2.3e-7, MUFU grade), 2^j added to the
-// exponent field.  x is clamped to >= -126 so the integer add cannot wrap (2^-126 is far below any
-// value that survives quantization).
-__device__ __forceinline__ f2 ex2_poly2(f2 x) {
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer in the low bits
-  x.x = fmaxf(x.x, -126.0f);
-  x.y = fmaxf(x.y, -126.0f);
-  const f2 t = fadd2(x, make_float2(kMagic, kMagic));
-  const f2 jf = fadd2(t, make_float2(-kMagic, -kMagic));  // rint(x), exact
-  const f2 f = fadd2(x, make_float2(-jf.x, -jf.y));       // x - rint(x), exact (Sterbenz)
-#if SAGE3_POLY_DEGREE == 3
-  // degree 3 (max rel. error 7.5e-5)
-  f2 p = make_float2(0.055171605199575424f, 0.055171605199575424f);
-  p = ffma2(p, f, make_float2(0.2426111400127411f, 0.2426111400127411f));
-  p = ffma2(p, f, make_float2(0.6932610273361206f, 0.6932610273361206f));
-  p = ffma2(p, f, make_float2(0.9999280571937561f, 0.9999280571937561f));
-#elif SAGE3_POLY_DEGREE == 4
-  // degree 4 (max rel. error 2.7e-6: below the E2M1 decision noise, reading c14)
-  f2 p = make_float2(0.009570094756782055f, 0.009570094756782055f);
-  p = ffma2(p, f, make_float2(0.05591786280274391f, 0.05591786280274391f));
-  p = ffma2(p, f, make_float2(0.240247443318367f, 0.240247443318367f));
-  p = ffma2(p, f, make_float2(0.6931217908859253f, 0.6931217908859253f));
-  p = ffma2(p, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
-#else
-  f2 p = make_float2(0.001327647129073739f, 0.001327647129073739f);
-  p = ffma2(p, f, make_float2(0.009675541892647743f, 0.009675541892647743f));
-  p = ffma2(p, f, make_float2(0.05550713464617729f, 0.05550713464617729f));
-  p = ffma2(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
-  p = ffma2(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
-  p = ffma2(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
-#endif
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-
-template <uint32_t N>
-__device__ __forceinline__ void setmaxnreg_dec() {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
-}
-template <uint32_t N>
-__device__ __forceinline__ void setmaxnreg_inc() {
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
-}
-
-// tcgen05.wait::ld that also orders the 32 destination registers (they are "+r" operands).
-__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
-                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
-                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
-                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
-               :
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
-                 "+r"(r[15])
-               :
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  tmem_ld_32x32b_x16(taddr, v);
-  tmem_ld_wait_regs(v);
-}
-
-__device__ __forceinline__ uint64_t sf_desc(const void* p) {
-  return make_smem_desc(smem_u32(p), 0, 128, kLayoutNone);
-}
-
-// max of 16 floats as a 3-input tree (FMNMX3)
-__device__ __forceinline__ float max16(const float* v) {
-  const float a = fmax3(v[0], v[1], v[2]), b = fmax3(v[3], v[4], v[5]), c = fmax3(v[6], v[7], v[8]);
-  const float d = fmax3(v[9], v[10], v[11]), e = fmax3(v[12], v[13], v[14]);
-  return fmax3(fmax3(a, b, c), fmax3(d, e, v[15]), -INFINITY);
-}
-
-#ifdef SAGE3_TRACE
-// Debug-only timeline: clock64 stamps per role r (1,2 softmax WGs, 4 correction, 5 S-MMA, 6 PV-MMA), KV tile
-// j < 128 and event k < 8, recorded by one thread per role in the CTAs with blockIdx.y == 0, blockIdx.x < 2.
-__device__ unsigned long long g_trace[2][8][128][8];
-#define SAGE3_TRACE_EV(role, j, k)                                                              \
-  do {                                                                                         \
-    if (blockIdx.y == 0 && blockIdx.x < 2 && ((threadIdx.x & 127) == 0 || threadIdx.x == 32 || threadIdx.x == 64) && (j) < 128) \
-      g_trace[blockIdx.x][role][j][k] = clock64();                                             \
-  } while (0)
-// per-warp variant: lane 0 of each warp of the role's warpgroup records event k0 + (warp & 3)
-#define SAGE3_TRACE_WARP(role, j, k0)                                                           \
-  do {                                                                                         \
-    if (blockIdx.y == 0 && blockIdx.x < 2 && (threadIdx.x & 31) == 0 && (j) < 128)               \
-      g_trace[blockIdx.x][role][j][(k0) + ((threadIdx.x >> 5) & 3)] = clock64();               \
-  } while (0)
-#else
-#define SAGE3_TRACE_WARP(role, j, k0) \
-  do {                                \
-  } while (0)
-#define SAGE3_TRACE_EV(role, j, k) \
-  do {                             \
-  } while (0)
-#endif
 
 // kSQ: smoothing Q (S += ds, Alg1 L8's GEMV term).  kMX: MXFP4 operands (Tab1a ablation): scale_vec::2X MMAs
 // with UE8M0 scales, P̂2 in 32-key blocks whose scale is the smallest power of two >= amax/6 (reading m1).
@@ -751,34 +630,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------- host
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
-// 2D uint8 map: rows of `row_bytes`, box = box_bytes x box_rows, swizzle matching the UMMA layout.
-bool make_map(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t rows, uint32_t box_bytes,
-              uint32_t box_rows) {
-  auto enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {row_bytes, rows};
-  cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {box_bytes, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  const CUtensorMapSwizzle swz = box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int D, bool kSQ, bool kMX, bool kDirect>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
   using L = Layout<D, kMX>;

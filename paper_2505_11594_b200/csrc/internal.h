@@ -48,5 +48,7 @@ struct AttnArgs {
 
 // Returns cudaSuccess or the launch / driver error.  `drv_err` receives a CUresult on descriptor failure.
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream);
+// The NEXT #2 lazy-reference variant (attn_lazy.cu; p_quant = SAGE3_P_TWO_LEVEL_LAZY, no smoothing Q).
+cudaError_t launch_attention_lazy(const AttnArgs& a, cudaStream_t stream);
 
 }  // namespace sage3
