@@ -24,6 +24,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sage3_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "sagebwd_oracle.c")]  # + SageBwd, Alg 2-3 (NEXT #3)
 _LIB = os.path.join(_HERE, "liboracle.so")
 _CFLAGS = ["-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC"]
 _lock = threading.Lock()
@@ -34,9 +35,9 @@ PMODE_TWO_LEVEL, PMODE_DIRECT, PMODE_NONE, PMODE_LAZY = 0, 1, 2, 3  # LAZY: NEXT
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (no fast-math, no FMA contraction, no FTZ/DAZ)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.run(["gcc", *_CFLAGS, _SRC, "-o", tmp, "-lm"], check=True)
+        subprocess.run(["gcc", *_CFLAGS, *_SRCS, "-o", tmp, "-lm"], check=True)
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -90,6 +91,14 @@ def lib():
                                                      ctypes.c_double, ip, ctypes.c_int, dp]
             L.oracle_num_threads.restype = ctypes.c_int
             L.oracle_e2m1_encode_array.argtypes = [fp, ctypes.c_int64, u8p]
+            i8p = ctypes.POINTER(ctypes.c_int8)
+            L.sb_psi.restype = ctypes.c_float
+            L.sb_psi.argtypes = [fp, ctypes.c_int, ctypes.c_int, i8p]
+            L.sb_quantize_head.argtypes = [fp, fp, fp, ctypes.c_int, ctypes.c_int, i8p, i8p, i8p, fp, fp, fp, fp]
+            L.sb_attn_fwd.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i8p, i8p, i8p, fp, fp, fp,
+                                      ctypes.c_int, ctypes.c_double, ip, ctypes.c_int, dp, dp]
+            L.sb_bwd_head.argtypes = [ctypes.c_int, ctypes.c_int, i8p, i8p, fp, fp, fp, fp, fp, fp, fp,
+                                      ctypes.c_int, ctypes.c_double, dp, dp, dp]
             L.oracle_e4m3_encode_array.argtypes = [fp, ctypes.c_int64, u8p]
             _lib = L
     return _lib
@@ -334,3 +343,68 @@ def accuracy_metrics(ref, test) -> dict:
     l1 = float(np.abs(a - b).sum() / np.abs(a).sum())
     rmse = float(np.sqrt(np.mean((a - b) ** 2)))
     return {"cos_sim": cos, "l1": l1, "rmse": rmse}
+
+
+# ------------------------------------------------------------------------------ SageBwd (NEXT #3)
+class SbHead:
+    """One head of SageBwd's INT8 per-block quantization (Alg2 L2 + L4): q, k, v int8 [Np][d], one fp32 scale
+    per 128-token block (sq, sk, sv [Np/128]), the smooth-K mean km [d]."""
+
+    def __init__(self, N, d):
+        Np = (N + 127) // 128 * 128
+        self.N, self.d, self.Np = N, d, Np
+        self.q = np.zeros((Np, d), np.int8)
+        self.k = np.zeros((Np, d), np.int8)
+        self.v = np.zeros((Np, d), np.int8)
+        self.sq = np.zeros(Np // 128, np.float32)
+        self.sk = np.zeros(Np // 128, np.float32)
+        self.sv = np.zeros(Np // 128, np.float32)
+        self.km = np.zeros(d, np.float32)
+
+
+def sb_psi(x) -> tuple[np.ndarray, float]:
+    """ψ of one block (reading b1): (int8 codes, scale)."""
+    x = _f32(x).reshape(-1)
+    q = np.zeros(x.shape[0], np.int8)
+    s = lib().sb_psi(_p(x, ctypes.c_float), x.shape[0], 1, _p(q, ctypes.c_int8))
+    return q, float(s)
+
+
+def sb_quantize_head(Q, K, V) -> SbHead:
+    """Alg2 L2 (smooth-K) + L4 (ψ per 128-token block of Q, K, V) for one head of 16-bit values."""
+    Q, K, V = _f32(Q), _f32(K), _f32(V)
+    N, d = Q.shape
+    h = SbHead(N, d)
+    lib().sb_quantize_head(_p(Q, ctypes.c_float), _p(K, ctypes.c_float), _p(V, ctypes.c_float), N, d,
+                           _p(h.q, ctypes.c_int8), _p(h.k, ctypes.c_int8), _p(h.v, ctypes.c_int8),
+                           _p(h.sq, ctypes.c_float), _p(h.sk, ctypes.c_float), _p(h.sv, ctypes.c_float),
+                           _p(h.km, ctypes.c_float))
+    return h
+
+
+def sb_attn_fwd(heads: list[SbHead], *, causal: bool, scale: float, rows=None, want_lse: bool = False):
+    """Alg2 L6-L14 on quantized heads: O [BH][nrows][d] fp64 (and lse = scale·m + ln l)."""
+    N, d, Np = heads[0].N, heads[0].d, heads[0].Np
+    rows = np.arange(N, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    cat = lambda name: np.ascontiguousarray(np.concatenate([getattr(h, name) for h in heads]))  # noqa: E731
+    q, k, v, sq, sk, sv = (cat(n) for n in ("q", "k", "v", "sq", "sk", "sv"))
+    O = np.zeros((len(heads), len(rows), d), np.float64)
+    lse = np.zeros((len(heads), len(rows)), np.float64)
+    lib().sb_attn_fwd(len(heads), N, d, _p(q, ctypes.c_int8), _p(k, ctypes.c_int8), _p(v, ctypes.c_int8),
+                      _p(sq, ctypes.c_float), _p(sk, ctypes.c_float), _p(sv, ctypes.c_float), int(causal),
+                      float(scale), _p(rows, ctypes.c_int), len(rows), _p(O, ctypes.c_double),
+                      _p(lse, ctypes.c_double))
+    return (O, lse) if want_lse else O
+
+
+def sb_attn_bwd(h: SbHead, V16, O, dO, L, *, causal: bool, scale: float):
+    """Alg3 for one head: (dQ, dK, dV) [N][d] fp64.  V16 = the 16-bit V values (dP = dO·Vᵀ stays unquantized,
+    P:329), O / L = the forward's output and lse, dO the incoming gradient."""
+    V16, O, dO, L = _f32(V16), _f32(O), _f32(dO), _f32(L)
+    N, d = h.N, h.d
+    dQ, dK, dV = (np.zeros((N, d), np.float64) for _ in range(3))
+    lib().sb_bwd_head(N, d, _p(h.q, ctypes.c_int8), _p(h.k, ctypes.c_int8), _p(h.sq, ctypes.c_float),
+                      _p(h.sk, ctypes.c_float), _p(h.km, ctypes.c_float), _p(V16, ctypes.c_float),
+                      _p(O, ctypes.c_float), _p(dO, ctypes.c_float), _p(L, ctypes.c_float), int(causal),
+                      float(scale), _p(dQ, ctypes.c_double), _p(dK, ctypes.c_double), _p(dV, ctypes.c_double))
+    return dQ, dK, dV
