@@ -175,6 +175,41 @@ typedef struct {
 sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype,
                                const sage3_attn_options* opts, float* lse, void* stream);
 
+/* ---------------------------------------------------------------------------------------------------------
+ * SageBwd's 8-bit attention forward (§4, Algorithm 2).
+ * ψ (reading b1): per 128-token block of each head, s = fl32(max|X| · fl32(1/127)),
+ * X̂ = clamp(RNE(fl32(x · fl32(1/s))), ±127) (s = 0: zero codes); K smoothed first (Alg2 L2, the c10 mean).
+ *   q, k : int8 [B][H][N_pad][d]          v_t : int8 [B][H][d][N_pad] (V transposed: tokens contiguous)
+ *   s_q, s_k, s_v : fp32 [B][H][N_pad/128] k_mean : fp32 [B][H][d]
+ * Padding tokens hold zero codes.  sage3_int8_attn_fwd: S = MM(Q̂, K̂)·s_Q·s_K (int32-exact), online softmax,
+ * per-token P̂ = P̃/s_P with s_P = exp(scale(rowmax(S) - m))/127 (Alg2 L10), O += MM(P̂, V̂)·s_P·s_V, O/l and
+ * lse = scale·m + ln l (Alg2 L13-14) — tcgen05.mma.kind::i8 for both products.  N_pad/128 must be <= 1024.
+ * --------------------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t B, H, N, d, N_pad;
+  int8_t* q;
+  int8_t* k;
+  int8_t* v_t;
+  float* s_q;
+  float* s_k;
+  float* s_v;
+  float* k_mean;
+} sage3_int8_qkv;
+
+/* bytes[0..6] = q, k, v_t, s_q, s_k, s_v, k_mean.  SAGE3_ERR_INVALID_ARG for unsupported shapes. */
+sage3_status sage3_int8_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]);
+
+/* Alg2 L2 + L4.  q, k, v as in sage3_quantize_qkv; workspace of sage3_quantize_workspace_bytes() bytes (the
+ * K-mean partial sums); nonfinite_flag nullable (OR-set to 1 on NaN/Inf input).  Bit-exact with the oracle's
+ * sb_quantize_head. */
+sage3_status sage3_int8_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 v, sage3_dtype in_dtype, int B,
+                                     int H, int N, int d, sage3_int8_qkv* out, void* workspace,
+                                     size_t workspace_bytes, uint32_t* nonfinite_flag, void* stream);
+
+/* Alg2 L6-L14 on *qkv; o, o_dtype, causal, softmax_scale, lse as in sage3_attn_fwd. */
+sage3_status sage3_int8_attn_fwd(const sage3_int8_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                                 float softmax_scale, float* lse, void* stream);
+
 /* End-to-end convenience path with HOST buffers (for e2e measurements): copies contiguous host
  * q, k, v ([B][H][N][d], in_dtype; pinned memory recommended) to device scratch, quantizes, runs the
  * attention and copies O (contiguous [B][H][N][d], o_dtype) back to o_host.  The work is split into up to

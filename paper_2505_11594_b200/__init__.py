@@ -29,7 +29,7 @@ _DT = {torch.float16: SAGE3_FP16, torch.bfloat16: SAGE3_BF16, torch.float32: SAG
 ABI_FUNCTIONS = (
     "sage3_fp4_qkv_sizes", "sage3_fp4_qkv_sizes_fmt", "sage3_smooth_q_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
     "sage3_attn_fwd", "sage3_attn_fwd_units", "sage3_attn_fwd_ex", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
-    "sage3_last_cuda_error", "sage3_version",
+    "sage3_last_cuda_error", "sage3_version", "sage3_int8_qkv_sizes", "sage3_int8_quantize_qkv", "sage3_int8_attn_fwd",
 )
 
 
@@ -46,6 +46,12 @@ class FP4QKVStruct(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("N", ctypes.c_int32), ("d", ctypes.c_int32),
                 ("N_pad", ctypes.c_int32), ("fmt", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in (
                     "q_data", "k_data", "v_data", "q_sf", "k_sf", "v_sf", "k_mean", "q_mean", "ds")]
+
+
+class INT8QKVStruct(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("N", ctypes.c_int32), ("d", ctypes.c_int32),
+                ("N_pad", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in (
+                    "q", "k", "v_t", "s_q", "s_k", "s_v", "k_mean")]
 
 
 class AttnOptions(ctypes.Structure):
@@ -87,6 +93,12 @@ def load() -> ctypes.CDLL:
     L.sage3_forward_host.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 6 + [ctypes.c_float, ctypes.c_void_p,
                                                                                 ctypes.c_int, ctypes.c_void_p, sz,
                                                                                 ctypes.c_void_p]
+    L.sage3_int8_qkv_sizes.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(sz)]
+    L.sage3_int8_quantize_qkv.argtypes = [Tensor4, Tensor4, Tensor4, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, ctypes.POINTER(INT8QKVStruct), ctypes.c_void_p,
+                                          sz, ctypes.c_void_p, ctypes.c_void_p]
+    L.sage3_int8_attn_fwd.argtypes = [ctypes.POINTER(INT8QKVStruct), Tensor4, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p]
     L.sage3_status_str.argtypes = [ctypes.c_int]
     L.sage3_status_str.restype = ctypes.c_char_p
     L.sage3_version.restype = ctypes.c_char_p
@@ -264,6 +276,56 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
     qkv = sage3_quantize_qkv(q, k, v, stream=stream, smooth_q=smooth_q, fmt=fmt)
     return sage3_attn_fwd(qkv, causal=causal, softmax_scale=softmax_scale, out_dtype=out_dtype or q.dtype,
                           stream=stream, p_quant=p_quant)
+
+
+# ------------------------------------------------------------------ SageBwd 8-bit forward (NEXT #3)
+def sage3_int8_qkv_sizes(B: int, H: int, N: int, d: int) -> list[int]:
+    out = (ctypes.c_size_t * 7)()
+    _check(load().sage3_int8_qkv_sizes(B, H, N, d, out), "sage3_int8_qkv_sizes")
+    return list(out)
+
+
+class INT8QKV:
+    """Device buffers of SageBwd's INT8 Q/K/V (include/sage3.h sage3_int8_qkv), allocated with torch."""
+
+    NAMES = ("q", "k", "v_t", "s_q", "s_k", "s_v", "k_mean")
+
+    def __init__(self, B: int, H: int, N: int, d: int, device):
+        self.B, self.H, self.N, self.d = B, H, N, d
+        self.N_pad = (N + 127) // 128 * 128
+        for name, nbytes in zip(self.NAMES, sage3_int8_qkv_sizes(B, H, N, d)):
+            setattr(self, name, torch.empty(nbytes, dtype=torch.uint8, device=device))
+        self.workspace = torch.empty(max(sage3_quantize_workspace_bytes(B, H, N, d), 16), dtype=torch.uint8,
+                                     device=device)
+        self.struct = INT8QKVStruct(B, H, N, d, self.N_pad, *[getattr(self, n).data_ptr() for n in self.NAMES])
+
+
+def sage3_int8_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: INT8QKV | None = None,
+                            nonfinite: torch.Tensor | None = None, stream=None) -> INT8QKV:
+    """Alg2 L2 + L4: smooth-K and per-block INT8 ψ of Q, K, V (see include/sage3.h)."""
+    B, H, N, d = q.shape
+    assert k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dtype in (torch.float16, torch.bfloat16)
+    if out is None:
+        out = INT8QKV(B, H, N, d, q.device)
+    flag = ctypes.c_void_p(nonfinite.data_ptr() if nonfinite is not None else None)
+    st = load().sage3_int8_quantize_qkv(_t4(q), _t4(k), _t4(v), _DT[q.dtype], B, H, N, d, ctypes.byref(out.struct),
+                                        ctypes.c_void_p(out.workspace.data_ptr()), out.workspace.numel(), flag,
+                                        _stream(stream))
+    _check(st, "sage3_int8_quantize_qkv")
+    return out
+
+
+def sage3_int8_attn_fwd(qkv: INT8QKV, o: torch.Tensor | None = None, *, causal: bool = False,
+                        softmax_scale: float = 0.0, lse: torch.Tensor | None = None, out_dtype=torch.bfloat16,
+                        stream=None) -> torch.Tensor:
+    """Alg2 L6-L14 (INT8 QKᵀ, online softmax, per-token INT8 P, INT8 PV, O/l, lse)."""
+    if o is None:
+        o = torch.empty(qkv.B, qkv.H, qkv.N, qkv.d, dtype=out_dtype, device=qkv.q.device)
+    lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
+    st = load().sage3_int8_attn_fwd(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], 1 if causal else 0,
+                                    float(softmax_scale), lse_p, _stream(stream))
+    _check(st, "sage3_int8_attn_fwd")
+    return o
 
 
 def default_scale(d: int) -> float:

@@ -220,6 +220,69 @@ sage3_status sage3_attn_fwd(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_dty
                               (int64_t)qkv->B * qkv->H * (npad(qkv->N) / 128), stream);
 }
 
+// ---------------------------------------------------------------------------------- SageBwd INT8 forward
+static bool i8_shape_ok(int B, int H, int N, int d) { return shape_ok(B, H, N, d) && npad(N) / 128 <= 1024; }
+
+sage3_status sage3_int8_qkv_sizes(int B, int H, int N, int d, size_t bytes[7]) {
+  if (!bytes || !i8_shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
+  const size_t BH = (size_t)B * H, Np = (size_t)npad(N);
+  bytes[0] = bytes[1] = bytes[2] = BH * Np * d;
+  bytes[3] = bytes[4] = bytes[5] = BH * (Np / 128) * sizeof(float);
+  bytes[6] = BH * d * sizeof(float);
+  return SAGE3_OK;
+}
+
+sage3_status sage3_int8_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_tensor4 v, sage3_dtype in_dtype, int B,
+                                     int H, int N, int d, sage3_int8_qkv* out, void* workspace,
+                                     size_t workspace_bytes, uint32_t* nonfinite_flag, void* stream) {
+  if (!out || !i8_shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
+  if (in_dtype != SAGE3_FP16 && in_dtype != SAGE3_BF16) return SAGE3_ERR_UNSUPPORTED;
+  if (!tensor_ok(q, 2) || !tensor_ok(k, 2) || !tensor_ok(v, 2)) return SAGE3_ERR_INVALID_ARG;
+  if (out->B != B || out->H != H || out->N != N || out->d != d) return SAGE3_ERR_INVALID_ARG;
+  if (!out->q || !out->k || !out->v_t || !out->s_q || !out->s_k || !out->s_v || !out->k_mean)
+    return SAGE3_ERR_INVALID_ARG;
+  if (!aligned16(out->q) || !aligned16(out->k) || !aligned16(out->v_t) || !aligned16(out->k_mean))
+    return SAGE3_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < sage3_quantize_workspace_bytes(B, H, N, d)) return SAGE3_ERR_WORKSPACE;
+  sage3_status st = device_ok();
+  if (st != SAGE3_OK) return st;
+  out->N_pad = (int32_t)npad(N);
+  sage3::I8Args a{};
+  a.q = q.ptr, a.k = k.ptr, a.v = v.ptr;
+  a.q_sb = q.stride_b, a.q_sh = q.stride_h, a.q_sn = q.stride_n;
+  a.k_sb = k.stride_b, a.k_sh = k.stride_h, a.k_sn = k.stride_n;
+  a.v_sb = v.stride_b, a.v_sh = v.stride_h, a.v_sn = v.stride_n;
+  a.B = B, a.H = H, a.N = N, a.Np = out->N_pad, a.d = d;
+  a.q8 = out->q, a.k8 = out->k, a.vt8 = out->v_t, a.sq = out->s_q, a.sk = out->s_k, a.sv = out->s_v;
+  a.k_mean = out->k_mean;
+  a.nonfinite = nonfinite_flag;
+  cudaError_t e = sage3::launch_quantize_i8(a, in_dtype == SAGE3_BF16, static_cast<double*>(workspace),
+                                            static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
+}
+
+sage3_status sage3_int8_attn_fwd(const sage3_int8_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
+                                 float softmax_scale, float* lse, void* stream) {
+  if (!qkv || !i8_shape_ok(qkv->B, qkv->H, qkv->N, qkv->d) || qkv->N_pad != npad(qkv->N))
+    return SAGE3_ERR_INVALID_ARG;
+  if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
+  if (!tensor_ok(o, esize_of(o_dtype))) return SAGE3_ERR_INVALID_ARG;
+  if (!qkv->q || !qkv->k || !qkv->v_t || !qkv->s_q || !qkv->s_k || !qkv->s_v) return SAGE3_ERR_INVALID_ARG;
+  if (!aligned16(qkv->q) || !aligned16(qkv->k) || !aligned16(qkv->v_t)) return SAGE3_ERR_INVALID_ARG;
+  if (!std::isfinite(softmax_scale)) return SAGE3_ERR_INVALID_ARG;
+  sage3_status st = device_ok();
+  if (st != SAGE3_OK) return st;
+  sage3::I8AttnArgs a{};
+  a.q8 = qkv->q, a.k8 = qkv->k, a.vt8 = qkv->v_t, a.sq = qkv->s_q, a.sk = qkv->s_k, a.sv = qkv->s_v;
+  a.o = o.ptr, a.o_sb = o.stride_b, a.o_sh = o.stride_h, a.o_sn = o.stride_n, a.o_dtype = (int)o_dtype;
+  a.lse = lse;
+  a.B = qkv->B, a.H = qkv->H, a.N = qkv->N, a.Np = qkv->N_pad, a.d = qkv->d;
+  a.causal = causal ? 1 : 0;
+  a.scale = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)qkv->d);
+  cudaError_t e = sage3::launch_attention_i8(a, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
+}
+
 // ---------------------------------------------------------------------------------- host e2e path
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 

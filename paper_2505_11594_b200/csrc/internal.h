@@ -31,6 +31,33 @@ struct VArgs {
 // k_mean is QKArgs::k_mean (non-const alias for the writer).
 cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream);
 
+cudaError_t launch_kmean(const QKArgs& qk, bool bf16, double* ws, cudaStream_t stream);
+
+// SageBwd INT8 (NEXT #3; quant_i8.cu / attn_i8.cu)
+struct I8Args {
+  const void *q, *k, *v;
+  int64_t q_sb, q_sh, q_sn, k_sb, k_sh, k_sn, v_sb, v_sh, v_sn;
+  int B, H, N, Np, d;
+  int8_t *q8, *k8, *vt8;  // [BH][Np][d], [BH][Np][d], [BH][d][Np]
+  float *sq, *sk, *sv;    // [BH][Np/128]
+  float* k_mean;          // [BH][d]
+  uint32_t* nonfinite;
+};
+cudaError_t launch_quantize_i8(const I8Args& a, bool bf16, double* ws, cudaStream_t stream);
+
+struct I8AttnArgs {
+  const int8_t *q8, *k8, *vt8;
+  const float *sq, *sk, *sv;
+  void* o;
+  int64_t o_sb, o_sh, o_sn;
+  int o_dtype;
+  float* lse;
+  int B, H, N, Np, d;
+  int causal;
+  float scale;
+};
+cudaError_t launch_attention_i8(const I8AttnArgs& a, cudaStream_t stream);
+
 struct AttnArgs {
   const uint8_t *q_data, *k_data, *v_data, *q_sf, *k_sf, *v_sf;
   void* o;

@@ -507,6 +507,20 @@ cudaError_t launch_fmt(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, 
               : launch_t<__half, 64, kMX>(qk, v, ws, stream);
 }
 
+// The smoothing-K mean alone (Alg1 L2 / Alg2 L2, reading c10), for the INT8 (SageBwd) quantizer.
+cudaError_t launch_kmean(const QKArgs& qk, bool bf16, double* ws, cudaStream_t stream) {
+  const int BH = qk.B * qk.H;
+  dim3 grid(qk.Np / 128, BH);
+  if (bf16)
+    kmean_kernel<__nv_bfloat16><<<grid, qk.d / 2, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(qk.k), qk.k_sb,
+                                                                qk.k_sh, qk.k_sn, qk.H, qk.N, qk.d, ws);
+  else
+    kmean_kernel<__half><<<grid, qk.d / 2, 0, stream>>>(reinterpret_cast<const __half*>(qk.k), qk.k_sb, qk.k_sh,
+                                                         qk.k_sn, qk.H, qk.N, qk.d, ws);
+  kmean_final_kernel<<<(BH * qk.d * 32 + 255) / 256, 256, 0, stream>>>(ws, qk.Np / 128, qk.N, BH * qk.d, qk.k_mean);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, cudaStream_t stream) {
   return qk.mx ? launch_fmt<true>(qk, v, bf16, ws, stream) : launch_fmt<false>(qk, v, bf16, ws, stream);
 }
