@@ -1,0 +1,7 @@
+#!/bin/bash
+# compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize_case.py -> gpurun_out/sanitize_*.txt
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_case.py > gpurun_out/sanitize_$tool.txt 2>&1
+  echo "$tool rc=$?"; tail -3 gpurun_out/sanitize_$tool.txt
+done

@@ -1,5 +1,6 @@
 """Small end-to-end cases for compute-sanitizer (SURVEY §4 layer 7): quantize + attention (d 64/128, causal
-and not, ragged N, smoothing Q) through the C ABI, plus the host-buffer path.
+and not, ragged N, smoothing Q, MXFP4, direct and lazy P, SageBwd INT8 forward) through the C ABI, plus the
+host-buffer path.
   compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_case.py"""
 import os
 import sys
@@ -16,6 +17,11 @@ for d in (64, 128):
             Q, K, V = synth.make_qkv(1, 1, N, d, seed=N, dtype=torch.bfloat16, device="cuda")
             s3.attention(Q, K, V, causal=causal)
             s3.attention(Q, K, V, causal=causal, smooth_q=True)
+            s3.attention(Q, K, V, causal=causal, fmt="mxfp4")
+            s3.attention(Q, K, V, causal=causal, p_quant="direct")
+            s3.attention(Q, K, V, causal=causal, p_quant="lazy")
+            s3.attention(Q, K, V, causal=causal, fmt="mxfp4", p_quant="lazy")
+            s3.sage3_int8_attn_fwd(s3.sage3_int8_quantize_qkv(Q, K, V), causal=causal)
             torch.cuda.synchronize()
 Q, K, V = synth.make_qkv(1, 2, 300, 128, seed=1, dtype=torch.bfloat16, device="cpu")
 qh, kh, vh = (x.pin_memory() for x in (Q, K, V))
