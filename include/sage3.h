@@ -210,6 +210,27 @@ sage3_status sage3_int8_quantize_qkv(sage3_tensor4 q, sage3_tensor4 k, sage3_ten
 sage3_status sage3_int8_attn_fwd(const sage3_int8_qkv* qkv, sage3_tensor4 o, sage3_dtype o_dtype, int causal,
                                  float softmax_scale, float* lse, void* stream);
 
+/* Algorithm 3 (SageBwd backward; readings b1-b8 in DESIGN.md §3.1).
+ *   qkv       : the Q̂, K̂ codes, s_Q, s_K and k_mean written by sage3_int8_quantize_qkv (v_t / s_v unused)
+ *   v, dout   : [B][H][N][d] 16-bit (in_dtype) — the unquantized V and dO of the FP16 product dP = dO·Vᵀ
+ *   o         : [B][H][N][d] in o_dtype (fp16 / bf16 / fp32), the forward output used for D = rowsum(dO∘O)
+ *   lse       : [B][H][N] fp32 device, the forward's L = scale·m + ln l (sage3_int8_attn_fwd's lse)
+ *   dq, dk, dv: [B][H][N][d] outputs in grad_dtype (fp16 / bf16 / fp32), gradients w.r.t. the UNSMOOTHED
+ *               q, k, v; dQ includes the smooth-K term rowsum(dS)·K_m (Alg3 L10); dQ and dK carry the softmax
+ *               scale.  Rows >= N are not written.
+ *   workspace : device, 16-byte aligned, sage3_int8_bwd_workspace_bytes() bytes (ψ(dO) codes and scales,
+ *               D, L·log2 e, the fp32 dQ accumulator); contents on return are unspecified.
+ * Per (query tile i, key tile j) of 128 x 128: ψ(P_ij) and ψ(dS_ij) use one scale per tile, ψ(dO_i) one per
+ * 128-row block (readings b1, b6).  S, dV, dK and dQ products run as tcgen05.mma.kind::i8, dP as kind::f16.
+ * Errors: SAGE3_ERR_INVALID_ARG (null / misaligned pointers, shape), SAGE3_ERR_UNSUPPORTED (dtype, device),
+ * SAGE3_ERR_WORKSPACE, SAGE3_ERR_CUDA.  Enqueued on `stream` only (four launches: memset, prep, main, dQ
+ * finalize). */
+size_t sage3_int8_bwd_workspace_bytes(int B, int H, int N, int d);
+sage3_status sage3_int8_attn_bwd(const sage3_int8_qkv* qkv, sage3_tensor4 v, sage3_tensor4 o, sage3_dtype o_dtype,
+                                 sage3_tensor4 dout, sage3_dtype in_dtype, const float* lse, int causal,
+                                 float softmax_scale, sage3_tensor4 dq, sage3_tensor4 dk, sage3_tensor4 dv,
+                                 sage3_dtype grad_dtype, void* workspace, size_t workspace_bytes, void* stream);
+
 /* End-to-end convenience path with HOST buffers (for e2e measurements): copies contiguous host
  * q, k, v ([B][H][N][d], in_dtype; pinned memory recommended) to device scratch, quantizes, runs the
  * attention and copies O (contiguous [B][H][N][d], o_dtype) back to o_host.  The work is split into up to

@@ -30,6 +30,7 @@ ABI_FUNCTIONS = (
     "sage3_fp4_qkv_sizes", "sage3_fp4_qkv_sizes_fmt", "sage3_smooth_q_sizes", "sage3_quantize_workspace_bytes", "sage3_kv_tile", "sage3_quantize_qkv",
     "sage3_attn_fwd", "sage3_attn_fwd_units", "sage3_attn_fwd_ex", "sage3_forward_host_scratch_bytes", "sage3_forward_host", "sage3_status_str",
     "sage3_last_cuda_error", "sage3_version", "sage3_int8_qkv_sizes", "sage3_int8_quantize_qkv", "sage3_int8_attn_fwd",
+    "sage3_int8_bwd_workspace_bytes", "sage3_int8_attn_bwd",
 )
 
 
@@ -99,6 +100,11 @@ def load() -> ctypes.CDLL:
                                           sz, ctypes.c_void_p, ctypes.c_void_p]
     L.sage3_int8_attn_fwd.argtypes = [ctypes.POINTER(INT8QKVStruct), Tensor4, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p]
+    L.sage3_int8_bwd_workspace_bytes.argtypes = [ctypes.c_int] * 4
+    L.sage3_int8_bwd_workspace_bytes.restype = ctypes.c_size_t
+    L.sage3_int8_attn_bwd.argtypes = [ctypes.POINTER(INT8QKVStruct), Tensor4, Tensor4, ctypes.c_int, Tensor4,
+                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_float, Tensor4, Tensor4,
+                                      Tensor4, ctypes.c_int, ctypes.c_void_p, sz, ctypes.c_void_p]
     L.sage3_status_str.argtypes = [ctypes.c_int]
     L.sage3_status_str.restype = ctypes.c_char_p
     L.sage3_version.restype = ctypes.c_char_p
@@ -330,3 +336,28 @@ def sage3_int8_attn_fwd(qkv: INT8QKV, o: torch.Tensor | None = None, *, causal: 
 
 def default_scale(d: int) -> float:
     return 1.0 / math.sqrt(d)
+
+
+def sage3_int8_bwd_workspace_bytes(B: int, H: int, N: int, d: int) -> int:
+    return int(load().sage3_int8_bwd_workspace_bytes(B, H, N, d))
+
+
+def sage3_int8_attn_bwd(qkv: INT8QKV, v: torch.Tensor, o: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor, *,
+                        causal: bool = False, softmax_scale: float = 0.0, grad_dtype=torch.float32,
+                        dq: torch.Tensor | None = None, dk: torch.Tensor | None = None, dv: torch.Tensor | None = None,
+                        workspace: torch.Tensor | None = None, stream=None):
+    """Alg3 (SageBwd backward): returns (dq, dk, dv) w.r.t. the unsmoothed q, k, v (see include/sage3.h)."""
+    B, H, N, d = qkv.B, qkv.H, qkv.N, qkv.d
+    assert v.shape == dout.shape == o.shape == (B, H, N, d) and v.dtype == dout.dtype
+    assert lse.dtype == torch.float32 and lse.is_contiguous() and lse.numel() == B * H * N
+    mk = lambda t: t if t is not None else torch.empty(B, H, N, d, dtype=grad_dtype, device=v.device)
+    dq, dk, dv = mk(dq), mk(dk), mk(dv)
+    if workspace is None:
+        workspace = torch.empty(sage3_int8_bwd_workspace_bytes(B, H, N, d), dtype=torch.uint8, device=v.device)
+    st = load().sage3_int8_attn_bwd(ctypes.byref(qkv.struct), _t4(v), _t4(o), _DT[o.dtype], _t4(dout), _DT[v.dtype],
+                                    ctypes.c_void_p(lse.data_ptr()), 1 if causal else 0, float(softmax_scale),
+                                    _t4(dq), _t4(dk), _t4(dv), _DT[dq.dtype], ctypes.c_void_p(workspace.data_ptr()),
+                                    workspace.numel(), _stream(stream))
+    _check(st, "sage3_int8_attn_bwd")
+    return dq, dk, dv
+

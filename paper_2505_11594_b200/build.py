@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsage3.so")
-SOURCES = ["abi.cu", "quant.cu", "attn.cu", "attn_lazy.cu", "quant_i8.cu", "attn_i8.cu"]
+SOURCES = ["abi.cu", "quant.cu", "attn.cu", "attn_lazy.cu", "quant_i8.cu", "attn_i8.cu", "bwd_i8.cu"]
 HEADERS = ["sm100.cuh", "attn_common.cuh", "internal.h", os.path.join("..", "..", "include", "sage3.h")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

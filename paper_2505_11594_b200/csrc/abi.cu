@@ -283,6 +283,57 @@ sage3_status sage3_int8_attn_fwd(const sage3_int8_qkv* qkv, sage3_tensor4 o, sag
   return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
 }
 
+size_t sage3_int8_bwd_workspace_bytes(int B, int H, int N, int d) {
+  if (!i8_shape_ok(B, H, N, d)) return 0;
+  const size_t BH = (size_t)B * H, Np = (size_t)npad(N);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return al(BH * Np * d) + al(BH * (Np / 128) * 4) + 2 * al(BH * Np * 4) + al(BH * Np * d * 4);
+}
+
+sage3_status sage3_int8_attn_bwd(const sage3_int8_qkv* qkv, sage3_tensor4 v, sage3_tensor4 o, sage3_dtype o_dtype,
+                                 sage3_tensor4 dout, sage3_dtype in_dtype, const float* lse, int causal,
+                                 float softmax_scale, sage3_tensor4 dq, sage3_tensor4 dk, sage3_tensor4 dv,
+                                 sage3_dtype grad_dtype, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!qkv || !i8_shape_ok(qkv->B, qkv->H, qkv->N, qkv->d) || qkv->N_pad != npad(qkv->N)) return SAGE3_ERR_INVALID_ARG;
+  if (in_dtype != SAGE3_FP16 && in_dtype != SAGE3_BF16) return SAGE3_ERR_UNSUPPORTED;
+  if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
+  if (grad_dtype != SAGE3_FP16 && grad_dtype != SAGE3_BF16 && grad_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
+  if (!tensor_ok(v, 2) || !tensor_ok(dout, 2) || !tensor_ok(o, esize_of(o_dtype))) return SAGE3_ERR_INVALID_ARG;
+  const int ge = esize_of(grad_dtype);
+  if (!tensor_ok(dq, ge) || !tensor_ok(dk, ge) || !tensor_ok(dv, ge)) return SAGE3_ERR_INVALID_ARG;
+  if (!qkv->q || !qkv->k || !qkv->s_q || !qkv->s_k || !qkv->k_mean || !lse) return SAGE3_ERR_INVALID_ARG;
+  if (!aligned16(qkv->q) || !aligned16(qkv->k)) return SAGE3_ERR_INVALID_ARG;
+  if (!std::isfinite(softmax_scale)) return SAGE3_ERR_INVALID_ARG;
+  const int B = qkv->B, H = qkv->H, N = qkv->N, d = qkv->d;
+  if (!workspace || !aligned16(workspace) || workspace_bytes < sage3_int8_bwd_workspace_bytes(B, H, N, d))
+    return SAGE3_ERR_WORKSPACE;
+  sage3_status st = device_ok();
+  if (st != SAGE3_OK) return st;
+  const size_t BH = (size_t)B * H, Np = (size_t)npad(N);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  uint8_t* p = static_cast<uint8_t*>(workspace);
+  sage3::I8BwdArgs a{};
+  a.do8 = reinterpret_cast<int8_t*>(p), p += al(BH * Np * d);
+  a.sdo = reinterpret_cast<float*>(p), p += al(BH * (Np / 128) * 4);
+  a.lp = reinterpret_cast<float*>(p), p += al(BH * Np * 4);
+  a.dd = reinterpret_cast<float*>(p), p += al(BH * Np * 4);
+  a.dqacc = reinterpret_cast<float*>(p);
+  a.q8 = qkv->q, a.k8 = qkv->k, a.sq = qkv->s_q, a.sk = qkv->s_k, a.km = qkv->k_mean;
+  a.v = v.ptr, a.v_sb = v.stride_b, a.v_sh = v.stride_h, a.v_sn = v.stride_n;
+  a.o = o.ptr, a.o_sb = o.stride_b, a.o_sh = o.stride_h, a.o_sn = o.stride_n, a.o_dtype = (int)o_dtype;
+  a.dout = dout.ptr, a.do_sb = dout.stride_b, a.do_sh = dout.stride_h, a.do_sn = dout.stride_n;
+  a.in_bf16 = in_dtype == SAGE3_BF16 ? 1 : 0;
+  a.lse = lse;
+  a.dq = dq.ptr, a.dq_sb = dq.stride_b, a.dq_sh = dq.stride_h, a.dq_sn = dq.stride_n;
+  a.dk = dk.ptr, a.dk_sb = dk.stride_b, a.dk_sh = dk.stride_h, a.dk_sn = dk.stride_n;
+  a.dv = dv.ptr, a.dv_sb = dv.stride_b, a.dv_sh = dv.stride_h, a.dv_sn = dv.stride_n;
+  a.g_dtype = (int)grad_dtype;
+  a.B = B, a.H = H, a.N = N, a.Np = (int)Np, a.d = d, a.causal = causal ? 1 : 0;
+  a.scale = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)d);
+  cudaError_t e = sage3::launch_attention_bwd_i8(a, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SAGE3_OK : cuda_fail(e);
+}
+
 // ---------------------------------------------------------------------------------- host e2e path
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 

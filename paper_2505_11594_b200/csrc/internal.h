@@ -58,6 +58,26 @@ struct I8AttnArgs {
 };
 cudaError_t launch_attention_i8(const I8AttnArgs& a, cudaStream_t stream);
 
+// SageBwd backward (Alg3; bwd_i8.cu).  Workspace arrays: do8 [BH][Np][d] int8, sdo [BH][Np/128],
+// lp / dd [BH][Np] (L'·, D), dqacc [BH][Np][d] fp32.
+struct I8BwdArgs {
+  const int8_t *q8, *k8;
+  const float *sq, *sk, *km;
+  const void *v, *o, *dout;
+  int64_t v_sb, v_sh, v_sn, o_sb, o_sh, o_sn, do_sb, do_sh, do_sn;
+  int in_bf16;  // v, dout: 1 bf16, 0 fp16
+  int o_dtype;  // sage3_dtype of o
+  const float* lse;  // [BH][N]
+  void *dq, *dk, *dv;
+  int64_t dq_sb, dq_sh, dq_sn, dk_sb, dk_sh, dk_sn, dv_sb, dv_sh, dv_sn;
+  int g_dtype;  // sage3_dtype of the gradients
+  int B, H, N, Np, d, causal;
+  float scale;
+  int8_t* do8;
+  float *sdo, *lp, *dd, *dqacc;
+};
+cudaError_t launch_attention_bwd_i8(const I8BwdArgs& a, cudaStream_t stream);
+
 struct AttnArgs {
   const uint8_t *q_data, *k_data, *v_data, *q_sf, *k_sf, *v_sf;
   void* o;
