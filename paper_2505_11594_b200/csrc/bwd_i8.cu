@@ -42,11 +42,12 @@ namespace {
 using namespace ptx;
 
 constexpr int kBThreads = 512;
-constexpr uint32_t kBRegWG0 = 48, kBRegElem = 136, kBRegDV = 160, kBRegDK = 168;
+constexpr uint32_t kBRegWG0 = 40, kBRegElem = 136, kBRegDV = 160, kBRegDK = 176;
 static_assert(kBRegWG0 + kBRegElem + kBRegDV + kBRegDK <= 512, "register budget");
 constexpr uint32_t kMagicIB = 0x4B400000u;  // float 1.5·2^23 bits: int x + kMagicIB reinterpreted = 12582912 + x
 constexpr float kMagicFB = 12582912.0f;
 constexpr float kOne127B = 0x1.020408p-7f;  // fl32(1/127)
+constexpr int kDQBufs = 3;  // dQ staging buffers per WG3 warp
 constexpr uint32_t kColS0 = 0, kColY = 128, kColS1 = 256, kColW = 384;
 
 // kind::i8: D s32, A/B signed; a_mn / b_mn select MN-major operands (bits 15 / 16).
@@ -152,12 +153,13 @@ struct BLayout {
   static constexpr int oDOq = oDO + k16Tile;
   static constexpr int oP = oDOq + kI8Tile;        // P̂: 128 query rows x 128 keys
   static constexpr int oDS = oP + 128 * 128;       // dŜ: same layout
-  static constexpr int oDQ = oDS + 128 * 128;      // dQ staging: 2 x [128 rows][32 fp32] (SWIZZLE_128B)
-  static constexpr int oLD = oDQ + 2 * 16384;      // 2 stages x (L' [128], D [128]) fp32
+  static constexpr int oDQ = oDS + 128 * 128;      // dQ staging: 4 warps x kDQBufs x [32 rows][32 fp32]
+  static constexpr int oLD = oDQ + 4 * kDQBufs * 4096;      // 2 stages x (L' [128], D [128]) fp32
   static constexpr int oKm = oLD + 2 * 1024;       // K_m [D] fp32
   static constexpr int oX = oKm + 512;             // 4 slots x (s_P, s_dS, pad, rowsum(dS)[128] at +512)
   static constexpr int oRed = oX + 4 * 1024;       // 2 x 4 floats (tile amax reductions)
-  static constexpr int oBar = oRed + 64;
+  static constexpr int oScl = oRed + 64;           // s_Q[Np/128], s_dO[Np/128] of the head (<= 1024 each)
+  static constexpr int oBar = oScl + 2 * 4096;
   static constexpr int kNumBars = 1 + 2 + 2 + 2 + 2 + 2 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 2 + 4;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kSmemAlloc = oTmem + 16 + 1024;
@@ -235,7 +237,13 @@ __global__ void __launch_bounds__(kBThreads, 1)
     prefetch_tmap(&tm_dqacc);
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
+  float* s_sq = reinterpret_cast<float*>(smem + L::oScl);
+  float* s_sdo = s_sq + 1024;
   if (threadIdx.x < D) s_km[threadIdx.x] = a.km[(int64_t)bh * D + threadIdx.x];
+  for (int x = threadIdx.x; x < n_t; x += kBThreads) {
+    s_sq[x] = a.sq[(int64_t)bh * n_t + x];
+    s_sdo[x] = a.sdo[(int64_t)bh * n_t + x];
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -255,17 +263,21 @@ __global__ void __launch_bounds__(kBThreads, 1)
           tma_load_4d(smem + L::oV + x * 16384, &tm_v, kv_full, 64 * x, j * 128, h, b);
         for (int t = 0; t < nt; ++t) {
           const int i = i0 + t, st = t & 1;
+          SAGE3_TRACE_EV(3, t, 0);
           mbar_wait(&q_empty[st], ((uint32_t)(t >> 1) & 1u) ^ 1u);
+          SAGE3_TRACE_EV(3, t, 1);
           mbar_arrive_expect_tx(&q_full[st], L::kI8Tile + 1024);
           tma_load_2d(smem + L::oQ + st * L::kI8Tile, &tm_q, &q_full[st], 0, bh * a.Np + i * 128);
           bulk_load(smem + L::oLD + st * 1024, a.lp + (int64_t)bh * a.Np + i * 128, 512, &q_full[st]);
           bulk_load(smem + L::oLD + st * 1024 + 512, a.dd + (int64_t)bh * a.Np + i * 128, 512, &q_full[st]);
           mbar_wait(&do_full[1], ((uint32_t)t & 1u) ^ 1u);
+          SAGE3_TRACE_EV(3, t, 2);
           mbar_arrive_expect_tx(&do_full[0], L::k16Tile);
 #pragma unroll
           for (int x = 0; x < D / 64; ++x)
             tma_load_4d(smem + L::oDO + x * 16384, &tm_do, &do_full[0], 64 * x, i * 128, h, b);
           mbar_wait(&dq8_full[1], ((uint32_t)t & 1u) ^ 1u);
+          SAGE3_TRACE_EV(3, t, 3);
           mbar_arrive_expect_tx(&dq8_full[0], L::kI8Tile);
           tma_load_2d(smem + L::oDOq, &tm_dq8, &dq8_full[0], 0, bh * a.Np + i * 128);
         }
@@ -344,10 +356,15 @@ __global__ void __launch_bounds__(kBThreads, 1)
         issue_s(0);
         issue_dp(0);
         for (int t = 0; t < nt; ++t) {
+          SAGE3_TRACE_EV(2, t, 0);
           if (t + 1 < nt) issue_s(t + 1);
+          SAGE3_TRACE_EV(2, t, 1);
           issue_dv(t);
+          SAGE3_TRACE_EV(2, t, 2);
           issue_dkq(t);
+          SAGE3_TRACE_EV(2, t, 3);
           if (t + 1 < nt) issue_dp(t + 1);
+          SAGE3_TRACE_EV(2, t, 4);
         }
       }
       __syncwarp();
@@ -358,53 +375,63 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int r = threadIdx.x - 128;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     const float cl2 = a.scale * kLog2e;
-    const float* sqv = a.sq + (int64_t)bh * n_t;
     const uint32_t sP_row = smem_u32(smem + L::oP) + r * 128, sDS_row = smem_u32(smem + L::oDS) + r * 128;
     float* red_a = s_red;
     float* red_b = s_red + 4;
-    for (int t = 0; t < nt; ++t) {
+    const f2 mg2 = make_float2(kMagicFB, kMagicFB);
+    // One (i, j) tile.  Only the causal diagonal and the padded last KV tile need key masking: a separate
+    // instantiation keeps the selects out of the common path.
+    auto tile = [&](const int t, auto masked_tag) {
+      constexpr bool masked = decltype(masked_tag)::value;
       const int i = i0 + t, st = t & 1;
       const int q_row = i * 128 + r;
       const uint32_t tS = lane_base + (st ? kColS1 : kColS0), tY = lane_base + kColY;
+      SAGE3_TRACE_EV(1, t, 0);
       mbar_wait(&q_full[st], (uint32_t)(t >> 1) & 1u);
       const float* ld = reinterpret_cast<const float*>(smem + L::oLD + st * 1024);
       const float lp = ld[r], dr = ld[128 + r];
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_empty[st]);
-      const float c = cl2 * sqv[i] * sk_j;  // S·scale·log2 e = S_int·c
+      const float c = cl2 * s_sq[i] * sk_j;  // S·scale·log2 e = S_int·c
       const f2 c2 = make_float2(c, c), nl2 = make_float2(-lp, -lp);
-      // keys visible to this row in the tile: all, or [0, lim] on the causal diagonal / the padded last tile
-      const bool masked = (a.causal && i == j) || (j == n_t - 1 && a.N < a.Np);
-      const int lim = a.causal ? min(a.N - 1, q_row) - j * 128 : a.N - 1 - j * 128;
+      const int lim = a.causal ? min(a.N - 1, q_row) - j * 128 : a.N - 1 - j * 128;  // last visible key
       // ---- phase A: P = 2^(S·c − L'), written back over S (fp32); tile max of P
       mbar_wait(&s_full[st], (uint32_t)(t >> 1) & 1u);
+      SAGE3_TRACE_EV(1, t, 1);
       tc_fence_after();
       float pmax = 0.0f;
+      auto pchunk = [&](int ch, uint32_t(&v)[32]) {
 #pragma unroll
-      for (int cc = 0; cc < 4; cc += 2) {
+        for (int e = 0; e < 32; e += 2) {
+          f2 x = ffma2(i2f2b(v[e], v[e + 1]), c2, nl2);
+          if constexpr (masked) {
+            x.x = (32 * ch + e > lim) ? -INFINITY : x.x;
+            x.y = (32 * ch + e + 1 > lim) ? -INFINITY : x.y;
+          }
+          const f2 p = ((kPolyMask >> (e >> 1)) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          pmax = fmax3(pmax, p.x, p.y);
+          v[e] = __float_as_uint(p.x);
+          v[e + 1] = __float_as_uint(p.y);
+        }
+      };
+      {
         uint32_t va[32], vb[32];
-        tmem_ld_32x32b_x32(tS + 32 * cc, va);
-        tmem_ld_32x32b_x32(tS + 32 * cc + 32, vb);
+        tmem_ld_32x32b_x32(tS, va);
+        tmem_ld_32x32b_x32(tS + 32, vb);
         tmem_ld_wait_regs(va);
         tmem_ld_wait_regs(vb);
-        auto pchunk = [&](int ch, uint32_t(&v)[32]) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            f2 x = ffma2(i2f2b(v[e], v[e + 1]), c2, nl2);
-            if (masked) {
-              x.x = (32 * ch + e > lim) ? -INFINITY : x.x;
-              x.y = (32 * ch + e + 1 > lim) ? -INFINITY : x.y;
-            }
-            const float p0 = ex2(x.x), p1 = ex2(x.y);
-            pmax = fmax3(pmax, p0, p1);
-            v[e] = __float_as_uint(p0);
-            v[e + 1] = __float_as_uint(p1);
-          }
-        };
-        pchunk(cc, va);
-        pchunk(cc + 1, vb);
-        tmem_st_32x32b_x32(tS + 32 * cc, va);
-        tmem_st_32x32b_x32(tS + 32 * cc + 32, vb);
+        pchunk(0, va);
+        tmem_st_32x32b_x32(tS, va);
+        tmem_ld_32x32b_x32(tS + 64, va);  // in flight during chunk 1
+        pchunk(1, vb);
+        tmem_st_32x32b_x32(tS + 32, vb);
+        tmem_ld_32x32b_x32(tS + 96, vb);
+        tmem_ld_wait_regs(va);
+        tmem_ld_wait_regs(vb);
+        pchunk(2, va);
+        tmem_st_32x32b_x32(tS + 64, va);
+        pchunk(3, vb);
+        tmem_st_32x32b_x32(tS + 96, vb);
       }
       // tile amax (ψ(P), Alg3 L6): warp shuffle, then across the four warps
 #pragma unroll
@@ -415,19 +442,15 @@ __global__ void __launch_bounds__(kBThreads, 1)
       const float amax_p = fmax3(fmaxf(red_a[0], red_a[1]), red_a[2], red_a[3]);
       const float s_p = __fmul_rn(amax_p, kOne127B);
       const float rp = s_p != 0.0f ? __frcp_rn(s_p) : 0.0f;
+      SAGE3_TRACE_EV(1, t, 2);
       // ---- phase B: P̂ = RNE(P·(1/s_P)) -> smem; dS = P∘(dP − D) written over dP; rowsum(dS); tile max |dS|
       mbar_wait(dp_full, (uint32_t)t & 1u);
       mbar_wait(sp_empty, ((uint32_t)t & 1u) ^ 1u);
+      SAGE3_TRACE_EV(1, t, 3);
       tc_fence_after();
-      const f2 rp2 = make_float2(rp, rp), mg2 = make_float2(kMagicFB, kMagicFB), nd2 = make_float2(-dr, -dr);
+      const f2 rp2 = make_float2(rp, rp), nd2 = make_float2(-dr, -dr);
       float dsmax = 0.0f, rs = 0.0f;
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {  // 16 keys per step
-        uint32_t vp[16], vd[16];
-        tmem_ld_32x32b_x16(tS + 16 * cc, vp);
-        tmem_ld_32x32b_x16(tY + 16 * cc, vd);
-        tmem_ld_wait_regs(vp);
-        tmem_ld_wait_regs(vd);
+      auto bchunk = [&](int cc, const uint32_t(&vp)[16], uint32_t(&vd)[16]) {  // keys [16cc, 16cc+16)
         uint32_t w[4];
         f2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -447,13 +470,34 @@ __global__ void __launch_bounds__(kBThreads, 1)
           w[q] = pack4(pp[0], pp[1]);
         }
         rs += acc.x + acc.y;
-        // keys [16cc, 16cc+16) = 16-byte chunk cc of row r, SWIZZLE_128B (chunk ^= r & 7)
+        // 16-byte chunk cc of row r, SWIZZLE_128B (chunk ^= r & 7)
         sts_v4(sP_row + ((cc ^ (r & 7)) * 16), w[0], w[1], w[2], w[3]);
         tmem_st_32x32b_x16(tY + 16 * cc, vd);
+      };
+      {
+        uint32_t pa[16], da[16], pb[16], db[16];
+        tmem_ld_32x32b_x16(tS, pa);
+        tmem_ld_32x32b_x16(tY, da);
+#pragma unroll
+        for (int cc = 0; cc < 8; cc += 2) {  // the loads of chunk c+1 are in flight while chunk c is computed
+          tmem_ld_32x32b_x16(tS + 16 * cc + 16, pb);
+          tmem_ld_32x32b_x16(tY + 16 * cc + 16, db);
+          tmem_ld_wait_regs(pa);
+          tmem_ld_wait_regs(da);
+          bchunk(cc, pa, da);
+          tmem_ld_wait_regs(pb);  // already complete (waited above); orders the reads of pb, db
+          tmem_ld_wait_regs(db);
+          if (cc + 2 < 8) {
+            tmem_ld_32x32b_x16(tS + 16 * cc + 32, pa);
+            tmem_ld_32x32b_x16(tY + 16 * cc + 32, da);
+          }
+          bchunk(cc + 1, pb, db);
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      SAGE3_TRACE_EV(1, t, 4);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dsmax = fmaxf(dsmax, __shfl_xor_sync(0xffffffffu, dsmax, o));
       if (lane == 0) red_b[warp & 3] = dsmax;
@@ -469,34 +513,49 @@ __global__ void __launch_bounds__(kBThreads, 1)
         mbar_arrive(&x_full[t & 3]);
       }
       // ---- phase C: dŜ = RNE(dS·(1/s_dS)) -> smem (two's-complement bytes)
+      SAGE3_TRACE_EV(1, t, 5);
       mbar_wait(sds_empty, ((uint32_t)t & 1u) ^ 1u);
+      SAGE3_TRACE_EV(1, t, 6);
       const f2 rd2 = make_float2(rds, rds);
+      auto dchunk = [&](int ch, const uint32_t(&v)[32]) {
+        uint32_t w[8];
 #pragma unroll
-      for (int cc = 0; cc < 4; cc += 2) {
+        for (int q = 0; q < 8; ++q) {
+          const int e = 4 * q;
+          const f2 t0 = fadd2(fmul2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), rd2), mg2);
+          const f2 t1 = fadd2(fmul2(make_float2(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])), rd2), mg2);
+          w[q] = pack4(t0, t1);
+        }
+        sts_v4(sDS_row + (((2 * ch) ^ (r & 7)) * 16), w[0], w[1], w[2], w[3]);
+        sts_v4(sDS_row + (((2 * ch + 1) ^ (r & 7)) * 16), w[4], w[5], w[6], w[7]);
+      };
+      {
         uint32_t va[32], vb[32];
-        tmem_ld_32x32b_x32(tY + 32 * cc, va);
-        tmem_ld_32x32b_x32(tY + 32 * cc + 32, vb);
+        tmem_ld_32x32b_x32(tY, va);
+        tmem_ld_32x32b_x32(tY + 32, vb);
         tmem_ld_wait_regs(va);
         tmem_ld_wait_regs(vb);
-        auto dchunk = [&](int ch, const uint32_t(&v)[32]) {
-          uint32_t w[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int e = 4 * q;
-            const f2 t0 = fadd2(fmul2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), rd2), mg2);
-            const f2 t1 = fadd2(fmul2(make_float2(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])), rd2), mg2);
-            w[q] = pack4(t0, t1);
-          }
-          sts_v4(sDS_row + (((2 * ch) ^ (r & 7)) * 16), w[0], w[1], w[2], w[3]);
-          sts_v4(sDS_row + (((2 * ch + 1) ^ (r & 7)) * 16), w[4], w[5], w[6], w[7]);
-        };
-        dchunk(cc, va);
-        dchunk(cc + 1, vb);
+        dchunk(0, va);
+        tmem_ld_32x32b_x32(tY + 64, va);
+        dchunk(1, vb);
+        tmem_ld_32x32b_x32(tY + 96, vb);
+        tmem_ld_wait_regs(va);
+        tmem_ld_wait_regs(vb);
+        dchunk(2, va);
+        dchunk(3, vb);
       }
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      SAGE3_TRACE_EV(1, t, 7);
+    };
+    const bool pad_last = j == n_t - 1 && a.N < a.Np;
+    for (int t = 0; t < nt; ++t) {
+      if ((a.causal && i0 + t == j) || pad_last)
+        tile(t, std::true_type{});
+      else
+        tile(t, std::false_type{});
     }
   } else if (wg == 2) {
     // ---------------------------------------------------------------------------- dV_j accumulation (key rows)
@@ -510,9 +569,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
       const int i = i0 + t;
       mbar_wait(&x_full[t & 3], (uint32_t)(t >> 2) & 1u);
       const float s_p = reinterpret_cast<const float*>(smem + L::oX + (t & 3) * 1024)[0];
-      const float w = __fmul_rn(s_p, a.sdo[(int64_t)bh * n_t + i]);
+      const float w = __fmul_rn(s_p, s_sdo[i]);
       const f2 w2 = make_float2(w, w);
+      SAGE3_TRACE_EV(5, t, 0);
       mbar_wait(dvp_full, (uint32_t)t & 1u);
+      SAGE3_TRACE_EV(5, t, 1);
       tc_fence_after();
 #pragma unroll
       for (int cc = 0; cc < D / 16; ++cc) {
@@ -524,6 +585,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dvp_empty);
+      SAGE3_TRACE_EV(5, t, 2);
     }
     const int key = j * 128 + r;
     if (key < a.N) store_row<D>(a.dv, a.dv_sb, a.dv_sh, a.dv_sn, a.g_dtype, b, h, key, acc, 1.0f);
@@ -532,69 +594,86 @@ __global__ void __launch_bounds__(kBThreads, 1)
     setmaxnreg_inc<kBRegDK>();
     const int r = threadIdx.x - 384;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-    const float* sqv = a.sq + (int64_t)bh * n_t;
     f2 acc[D / 2];
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) acc[c] = make_float2(0.f, 0.f);
-    int nflush = 0;  // dQ staging chunks issued (buffer = nflush & 1)
+    // dQ staging: per warp, kDQBufs buffers of [32 rows][32 fp32] (4 KB, SWIZZLE_128B); each warp issues its
+    // own TMA reduce-adds (box 32 x 32), so no cross-warp barrier is needed
+    uint8_t* stage = smem + L::oDQ + (warp & 3) * (kDQBufs * 4096);
+    int nflush = 0;
     for (int t = 0; t < nt; ++t) {
       const int i = i0 + t, st = t & 1;
       mbar_wait(&x_full[t & 3], (uint32_t)(t >> 2) & 1u);
       const float* x = reinterpret_cast<const float*>(smem + L::oX + (t & 3) * 1024);
       const float s_ds = x[1], rs = x[128 + r];
-      const float wk = __fmul_rn(__fmul_rn(s_ds, sqv[i]), a.scale);  // dK carries the softmax scale (b7)
+      const float wk = __fmul_rn(__fmul_rn(s_ds, s_sq[i]), a.scale);  // dK carries the softmax scale (b7)
       const float wq = __fmul_rn(s_ds, sk_j);
+      SAGE3_TRACE_EV(4, t, 0);
       mbar_wait(kq_full, (uint32_t)t & 1u);
+      SAGE3_TRACE_EV(4, t, 1);
       tc_fence_after();
-      {
+      {  // dK partial (TMEM columns kColY..): two 16-column loads in flight
         const f2 w2 = make_float2(wk, wk);
 #pragma unroll
-        for (int cc = 0; cc < D / 16; ++cc) {
-          uint32_t v[16];
-          tmem_ld16(lane_base + kColY + 16 * cc, v);
+        for (int cc = 0; cc < D / 16; cc += 2) {
+          uint32_t va[16], vb[16];
+          tmem_ld_32x32b_x16(lane_base + kColY + 16 * cc, va);
+          tmem_ld_32x32b_x16(lane_base + kColY + 16 * cc + 16, vb);
+          tmem_ld_wait_regs(va);
+          tmem_ld_wait_regs(vb);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[8 * cc + e] = ffma2(i2f2b(v[2 * e], v[2 * e + 1]), w2, acc[8 * cc + e]);
+          for (int e = 0; e < 8; ++e) acc[8 * cc + e] = ffma2(i2f2b(va[2 * e], va[2 * e + 1]), w2, acc[8 * cc + e]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            acc[8 * cc + 8 + e] = ffma2(i2f2b(vb[2 * e], vb[2 * e + 1]), w2, acc[8 * cc + 8 + e]);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty);
+      SAGE3_TRACE_EV(4, t, 2);
       // dQ partial of (i, j): MM(dŜ, K̂_j)·s_dS·s_K + rowsum(dS)·K_m, 32 columns per TMA reduce-add
       const uint32_t tQ = lane_base + (st ? kColS1 : kColS0);
       const f2 wq2 = make_float2(wq, wq), rs2 = make_float2(rs, rs);
-#pragma unroll 1
-      for (int cc = 0; cc < D / 32; ++cc, ++nflush) {
-        const int buf = nflush & 1;
-        if (threadIdx.x == 384) bulk_wait_read<1>();  // the reduce that last read this buffer is done
-        named_bar(3, 128);
-        const uint32_t row = smem_u32(smem + L::oDQ + buf * 16384) + r * 128;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t v[16];
-          tmem_ld16(tQ + 32 * cc + 16 * hh, v);
+      for (int cc = 0; cc < D / 32; ++cc, ++nflush) {
+        uint8_t* buf = stage + (nflush % kDQBufs) * 4096;
+        uint32_t va[16], vb[16];
+        tmem_ld_32x32b_x16(tQ + 32 * cc, va);
+        tmem_ld_32x32b_x16(tQ + 32 * cc + 16, vb);
+        if (lane == 0) bulk_wait_read<kDQBufs - 1>();  // this warp's reduce that last read `buf` is done
+        __syncwarp();
+        tmem_ld_wait_regs(va);
+        tmem_ld_wait_regs(vb);
+        const uint32_t row = smem_u32(buf) + (r & 31) * 128;
+        auto put = [&](int hh, const uint32_t(&v)[16]) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int e = 4 * q, col = 32 * cc + 16 * hh + e;
-            const float2 k01 = *reinterpret_cast<const float2*>(s_km + col);
-            const float2 k23 = *reinterpret_cast<const float2*>(s_km + col + 2);
-            const f2 y0 = ffma2(i2f2b(v[e], v[e + 1]), wq2, fmul2(rs2, k01));
-            const f2 y1 = ffma2(i2f2b(v[e + 2], v[e + 3]), wq2, fmul2(rs2, k23));
+            const float4 km = *reinterpret_cast<const float4*>(s_km + col);
+            const f2 y0 = ffma2(i2f2b(v[e], v[e + 1]), wq2, fmul2(rs2, make_float2(km.x, km.y)));
+            const f2 y1 = ffma2(i2f2b(v[e + 2], v[e + 3]), wq2, fmul2(rs2, make_float2(km.z, km.w)));
             sts_v4(row + (((4 * hh + q) ^ (r & 7)) * 16), __float_as_uint(y0.x), __float_as_uint(y0.y),
                    __float_as_uint(y1.x), __float_as_uint(y1.y));
           }
-        }
+        };
+        put(0, va);
+        put(1, vb);
         fence_proxy_async_smem();
-        named_bar(4, 128);
-        if (threadIdx.x == 384) {
-          tma_reduce_add_2d(&tm_dqacc, smem + L::oDQ + buf * 16384, 32 * cc, bh * a.Np + i * 128);
+        __syncwarp();
+#ifndef SAGE3_BWD_NO_DQ_REDUCE  // (experiment: measures the cost of the dQ reduce-adds; wrong dQ)
+        if (lane == 0) {
+          tma_reduce_add_2d(&tm_dqacc, buf, 32 * cc, bh * a.Np + i * 128 + (warp & 3) * 32);
           bulk_commit();
         }
+#endif
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sb_empty[st]);
+      SAGE3_TRACE_EV(4, t, 3);
     }
-    if (threadIdx.x == 384) bulk_wait<0>();
+    if (lane == 0) bulk_wait<0>();
     const int key = j * 128 + r;
     if (key < a.N) store_row<D>(a.dk, a.dk_sb, a.dk_sh, a.dk_sn, a.g_dtype, b, h, key, acc, 1.0f);
   }
@@ -755,7 +834,7 @@ cudaError_t launch_bwd_d(const I8BwdArgs& a, cudaStream_t stream) {
   const uint64_t rows = (uint64_t)BH * a.Np;
   CUtensorMap tq, tk, tdq8, tv, tdo, tacc;
   const cuuint64_t adims[2] = {(cuuint64_t)D, rows}, astr[1] = {(cuuint64_t)D * 4};
-  const cuuint32_t abox[2] = {32, 128};
+  const cuuint32_t abox[2] = {32, 32};
   if (!map_i8(&tq, a.q8, D, rows) || !map_i8(&tk, a.k8, D, rows) || !map_i8(&tdq8, a.do8, D, rows) ||
       !map_16(&tv, a.v, a.B, a.H, a.N, D, a.v_sb, a.v_sh, a.v_sn) ||
       !map_16(&tdo, a.dout, a.B, a.H, a.N, D, a.do_sb, a.do_sh, a.do_sn) ||
@@ -776,5 +855,12 @@ cudaError_t launch_bwd_d(const I8BwdArgs& a, cudaStream_t stream) {
 cudaError_t launch_attention_bwd_i8(const I8BwdArgs& a, cudaStream_t stream) {
   return a.d == 128 ? launch_bwd_d<128>(a, stream) : launch_bwd_d<64>(a, stream);
 }
+
+#ifdef SAGE3_TRACE
+extern "C" int sage3_debug_trace_copy_bwd(void* host, size_t bytes) {
+  if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);
+  return (int)cudaMemcpyFromSymbol(host, g_trace, bytes);
+}
+#endif
 
 }  // namespace sage3
