@@ -142,6 +142,73 @@ __device__ __forceinline__ void store_row(void* base, int64_t sb, int64_t sh, in
   }
 }
 
+// One warp's share of a dQ partial: columns [c0, c0 + 16·NCH) of its 32 rows (TMEM lanes), scaled
+// y = int·w_q + rowsum(dS)·K_m, staged in smem ([32 rows][16 fp32], SWIZZLE_64B, kDQBufs buffers per warp)
+// and added into the fp32 dQ accumulator by this warp's own TMA reduce-adds (box 16 x 32).
+__device__ __forceinline__ void red_add_v4(float* gaddr, f2 a, f2 b) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gaddr), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y)
+               : "memory");
+}
+#ifndef SAGE3_BWD_DQ_TMA
+#define SAGE3_BWD_DQ_TMA 1
+#endif
+template <int NCH>
+__device__ __forceinline__ void flush_dq(const CUtensorMap* tm, uint32_t tQ, int c0, uint8_t* stage, int& nflush,
+                                         const float* s_km, f2 wq2, f2 rs2, int r, int lane, int row0,
+                                         float* dq_row) {
+  if constexpr (!SAGE3_BWD_DQ_TMA) {
+    // vector reductions straight from registers (red.global.add.v4.f32): no shared-memory traffic, which the
+    // MMAs' operand reads already saturate
+#pragma unroll
+    for (int k = 0; k < NCH; k += 2) {
+      uint32_t va[16], vb[16];
+      tmem_ld_32x32b_x16(tQ + c0 + 16 * k, va);
+      tmem_ld_32x32b_x16(tQ + c0 + 16 * k + 16, vb);
+      tmem_ld_wait_regs(va);
+      tmem_ld_wait_regs(vb);
+      auto put = [&](int kk, const uint32_t(&v)[16]) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int col = c0 + 16 * kk + 4 * q;
+          float4 km;
+          lds_f4(smem_u32(s_km + col), km);
+          const f2 y0 = ffma2(i2f2b(v[4 * q], v[4 * q + 1]), wq2, fmul2(rs2, make_float2(km.x, km.y)));
+          const f2 y1 = ffma2(i2f2b(v[4 * q + 2], v[4 * q + 3]), wq2, fmul2(rs2, make_float2(km.z, km.w)));
+          red_add_v4(dq_row + col, y0, y1);
+        }
+      };
+      put(k, va);
+      put(k + 1, vb);
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int k = 0; k < NCH; ++k, ++nflush) {
+    uint8_t* buf = stage + (nflush % kDQBufs) * 2048;
+    uint32_t v[16];
+    tmem_ld_32x32b_x16(tQ + c0 + 16 * k, v);
+    if (lane == 0) bulk_wait_read<kDQBufs - 1>();  // this warp's reduce that last read `buf` is done
+    __syncwarp();
+    tmem_ld_wait_regs(v);
+    const uint32_t row = smem_u32(buf) + (r & 31) * 64;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 km;
+      lds_f4(smem_u32(s_km + c0 + 16 * k + 4 * q), km);
+      const f2 y0 = ffma2(i2f2b(v[4 * q], v[4 * q + 1]), wq2, fmul2(rs2, make_float2(km.x, km.y)));
+      const f2 y1 = ffma2(i2f2b(v[4 * q + 2], v[4 * q + 3]), wq2, fmul2(rs2, make_float2(km.z, km.w)));
+      sts_v4(row + ((q ^ ((r >> 1) & 3)) * 16), __float_as_uint(y0.x), __float_as_uint(y0.y), __float_as_uint(y1.x),
+             __float_as_uint(y1.y));
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_reduce_add_2d(tm, buf, c0 + 16 * k, row0);
+      bulk_commit();
+    }
+  }
+}
+
 template <int D>
 struct BLayout {
   static constexpr int kI8Tile = 128 * D;         // Q̂ / K̂ / dÔ tile (row-major, D bytes per row)
@@ -153,8 +220,8 @@ struct BLayout {
   static constexpr int oDOq = oDO + k16Tile;
   static constexpr int oP = oDOq + kI8Tile;        // P̂: 128 query rows x 128 keys
   static constexpr int oDS = oP + 128 * 128;       // dŜ: same layout
-  static constexpr int oDQ = oDS + 128 * 128;      // dQ staging: 4 warps x kDQBufs x [32 rows][32 fp32]
-  static constexpr int oLD = oDQ + 4 * kDQBufs * 4096;      // 2 stages x (L' [128], D [128]) fp32
+  static constexpr int oDQ = oDS + 128 * 128;      // dQ staging: 8 warps x kDQBufs x [32 rows][16 fp32]
+  static constexpr int oLD = oDQ + 8 * kDQBufs * 2048;      // 2 stages x (L' [128], D [128]) fp32
   static constexpr int oKm = oLD + 2 * 1024;       // K_m [D] fp32
   static constexpr int oX = oKm + 512;             // 4 slots x (s_P, s_dS, pad, rowsum(dS)[128] at +512)
   static constexpr int oRed = oX + 4 * 1024;       // 2 x 4 floats (tile amax reductions)
@@ -210,7 +277,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 5);
       mbar_init(&s_full[s], 1);
-      mbar_init(&sb_empty[s], 4);
+      mbar_init(&sb_empty[s], 8);  // WG2 and WG3 warps (each flushes half of the dQ partial)
     }
     mbar_init(&do_full[0], 1);
     mbar_init(&do_full[1], 1);
@@ -388,56 +455,52 @@ __global__ void __launch_bounds__(kBThreads, 1)
       const uint32_t tS = lane_base + (st ? kColS1 : kColS0), tY = lane_base + kColY;
       SAGE3_TRACE_EV(1, t, 0);
       mbar_wait(&q_full[st], (uint32_t)(t >> 1) & 1u);
-      const float* ld = reinterpret_cast<const float*>(smem + L::oLD + st * 1024);
-      const float lp = ld[r], dr = ld[128 + r];
+      const uint32_t ld = smem_u32(smem + L::oLD + st * 1024) + 4 * r;
+      const float lp = lds_f32(ld), dr = lds_f32(ld + 512);
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_empty[st]);
       const float c = cl2 * s_sq[i] * sk_j;  // S·scale·log2 e = S_int·c
       const f2 c2 = make_float2(c, c), nl2 = make_float2(-lp, -lp);
       const int lim = a.causal ? min(a.N - 1, q_row) - j * 128 : a.N - 1 - j * 128;  // last visible key
-      // ---- phase A: P = 2^(S·c − L'), written back over S (fp32); tile max of P
+      // ---- phase A: the tile max of P = 2^(S·c − L') is 2^(rowmax(S_int)·c − L') maximised over the rows
+      //      (c > 0, exp monotone): an integer row max (3-input VIMNMX) and one exp per row; P itself is
+      //      computed once, in phase B, by the same instructions as this row maximum.
       mbar_wait(&s_full[st], (uint32_t)(t >> 1) & 1u);
       SAGE3_TRACE_EV(1, t, 1);
       tc_fence_after();
-      float pmax = 0.0f;
-      auto pchunk = [&](int ch, uint32_t(&v)[32]) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          f2 x = ffma2(i2f2b(v[e], v[e + 1]), c2, nl2);
-          if constexpr (masked) {
-            x.x = (32 * ch + e > lim) ? -INFINITY : x.x;
-            x.y = (32 * ch + e + 1 > lim) ? -INFINITY : x.y;
-          }
-          const f2 p = ((kPolyMask >> (e >> 1)) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          pmax = fmax3(pmax, p.x, p.y);
-          v[e] = __float_as_uint(p.x);
-          v[e + 1] = __float_as_uint(p.y);
-        }
-      };
+      int smax = INT_MIN;
       {
         uint32_t va[32], vb[32];
-        tmem_ld_32x32b_x32(tS, va);
-        tmem_ld_32x32b_x32(tS + 32, vb);
-        tmem_ld_wait_regs(va);
-        tmem_ld_wait_regs(vb);
-        pchunk(0, va);
-        tmem_st_32x32b_x32(tS, va);
-        tmem_ld_32x32b_x32(tS + 64, va);  // in flight during chunk 1
-        pchunk(1, vb);
-        tmem_st_32x32b_x32(tS + 32, vb);
-        tmem_ld_32x32b_x32(tS + 96, vb);
-        tmem_ld_wait_regs(va);
-        tmem_ld_wait_regs(vb);
-        pchunk(2, va);
-        tmem_st_32x32b_x32(tS + 64, va);
-        pchunk(3, vb);
-        tmem_st_32x32b_x32(tS + 96, vb);
+        auto rmax = [&](int ch, const uint32_t(&v)[32]) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            int x0 = (int)v[e], x1 = (int)v[e + 1];
+            if constexpr (masked) {
+              x0 = (32 * ch + e > lim) ? INT_MIN : x0;
+              x1 = (32 * ch + e + 1 > lim) ? INT_MIN : x1;
+            }
+            smax = __vimax3_s32(smax, x0, x1);
+          }
+        };
+#pragma unroll 1  // rolled loops keep the per-role code small (the four roles share each SM's i-cache)
+        for (int ch = 0; ch < 4; ch += 2) {
+          tmem_ld_32x32b_x32(tS + 32 * ch, va);
+          tmem_ld_32x32b_x32(tS + 32 * ch + 32, vb);
+          tmem_ld_wait_regs(va);
+          tmem_ld_wait_regs(vb);
+          rmax(ch, va);
+          rmax(ch + 1, vb);
+        }
+      }
+      float pmax;
+      {
+        const f2 x = ffma2(i2f2b((uint32_t)smax, (uint32_t)smax), c2, nl2);
+        pmax = smax == INT_MIN ? 0.0f : ex2(x.x);
       }
       // tile amax (ψ(P), Alg3 L6): warp shuffle, then across the four warps
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
       if (lane == 0) red_a[warp & 3] = pmax;
-      tmem_st_wait();
       named_bar(1, 128);
       const float amax_p = fmax3(fmaxf(red_a[0], red_a[1]), red_a[2], red_a[3]);
       const float s_p = __fmul_rn(amax_p, kOne127B);
@@ -450,7 +513,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tc_fence_after();
       const f2 rp2 = make_float2(rp, rp), nd2 = make_float2(-dr, -dr);
       float dsmax = 0.0f, rs = 0.0f;
-      auto bchunk = [&](int cc, const uint32_t(&vp)[16], uint32_t(&vd)[16]) {  // keys [16cc, 16cc+16)
+      auto bchunk = [&](int cc, const uint32_t(&vs)[16], uint32_t(&vd)[16]) {  // keys [16cc, 16cc+16)
         uint32_t w[4];
         f2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -459,7 +522,12 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int e = 4 * q + 2 * u;
-            const f2 p = make_float2(__uint_as_float(vp[e]), __uint_as_float(vp[e + 1]));
+            f2 x = ffma2(i2f2b(vs[e], vs[e + 1]), c2, nl2);  // Alg3 L5: P = exp(scale·S·s_Q·s_K − L)
+            if constexpr (masked) {
+              x.x = (16 * cc + e > lim) ? -INFINITY : x.x;
+              x.y = (16 * cc + e + 1 > lim) ? -INFINITY : x.y;
+            }
+            const f2 p = make_float2(ex2(x.x), ex2(x.y));
             pp[u] = fadd2(fmul2(p, rp2), mg2);
             const f2 ds = fmul2(p, fadd2(make_float2(__uint_as_float(vd[e]), __uint_as_float(vd[e + 1])), nd2));
             acc = fadd2(acc, ds);
@@ -478,7 +546,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
         uint32_t pa[16], da[16], pb[16], db[16];
         tmem_ld_32x32b_x16(tS, pa);
         tmem_ld_32x32b_x16(tY, da);
-#pragma unroll
+#pragma unroll 1
         for (int cc = 0; cc < 8; cc += 2) {  // the loads of chunk c+1 are in flight while chunk c is computed
           tmem_ld_32x32b_x16(tS + 16 * cc + 16, pb);
           tmem_ld_32x32b_x16(tY + 16 * cc + 16, db);
@@ -531,18 +599,15 @@ __global__ void __launch_bounds__(kBThreads, 1)
       };
       {
         uint32_t va[32], vb[32];
-        tmem_ld_32x32b_x32(tY, va);
-        tmem_ld_32x32b_x32(tY + 32, vb);
-        tmem_ld_wait_regs(va);
-        tmem_ld_wait_regs(vb);
-        dchunk(0, va);
-        tmem_ld_32x32b_x32(tY + 64, va);
-        dchunk(1, vb);
-        tmem_ld_32x32b_x32(tY + 96, vb);
-        tmem_ld_wait_regs(va);
-        tmem_ld_wait_regs(vb);
-        dchunk(2, va);
-        dchunk(3, vb);
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ch += 2) {
+          tmem_ld_32x32b_x32(tY + 32 * ch, va);
+          tmem_ld_32x32b_x32(tY + 32 * ch + 32, vb);
+          tmem_ld_wait_regs(va);
+          tmem_ld_wait_regs(vb);
+          dchunk(ch, va);
+          dchunk(ch + 1, vb);
+        }
       }
       fence_proxy_async_smem();
       tc_fence_before();
@@ -559,16 +624,21 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
   } else if (wg == 2) {
     // ---------------------------------------------------------------------------- dV_j accumulation (key rows)
+    //                                                                              + dQ partial columns [0, D/2)
     setmaxnreg_inc<kBRegDV>();
     const int r = threadIdx.x - 256;
-    const uint32_t tW = tbase + ((uint32_t)((warp & 3) * 32) << 16) + kColW;
+    const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t tW = lane_base + kColW;
+    uint8_t* stage = smem + L::oDQ + (warp & 3) * (kDQBufs * 2048);
+    int nflush = 0;
     f2 acc[D / 2];
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) acc[c] = make_float2(0.f, 0.f);
     for (int t = 0; t < nt; ++t) {
-      const int i = i0 + t;
+      const int i = i0 + t, st = t & 1;
       mbar_wait(&x_full[t & 3], (uint32_t)(t >> 2) & 1u);
-      const float s_p = reinterpret_cast<const float*>(smem + L::oX + (t & 3) * 1024)[0];
+      const uint32_t xs = smem_u32(smem + L::oX + (t & 3) * 1024);
+      const float s_p = lds_f32(xs), s_ds = lds_f32(xs + 4), rs = lds_f32(xs + 512 + 4 * r);
       const float w = __fmul_rn(s_p, s_sdo[i]);
       const f2 w2 = make_float2(w, w);
       SAGE3_TRACE_EV(5, t, 0);
@@ -586,7 +656,18 @@ __global__ void __launch_bounds__(kBThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(dvp_empty);
       SAGE3_TRACE_EV(5, t, 2);
+      const float wq = __fmul_rn(s_ds, sk_j);
+      mbar_wait(kq_full, (uint32_t)t & 1u);
+      tc_fence_after();
+      flush_dq<D / 32>(&tm_dqacc, lane_base + (st ? kColS1 : kColS0), 0, stage, nflush, s_km, make_float2(wq, wq),
+                       make_float2(rs, rs), r, lane, bh * a.Np + i * 128 + (warp & 3) * 32,
+                       a.dqacc + ((int64_t)bh * a.Np + i * 128 + r) * D);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sb_empty[st]);
+      SAGE3_TRACE_EV(5, t, 3);
     }
+    if (lane == 0) bulk_wait<0>();
     const int key = j * 128 + r;
     if (key < a.N) store_row<D>(a.dv, a.dv_sb, a.dv_sh, a.dv_sn, a.g_dtype, b, h, key, acc, 1.0f);
   } else {
@@ -597,15 +678,13 @@ __global__ void __launch_bounds__(kBThreads, 1)
     f2 acc[D / 2];
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) acc[c] = make_float2(0.f, 0.f);
-    // dQ staging: per warp, kDQBufs buffers of [32 rows][32 fp32] (4 KB, SWIZZLE_128B); each warp issues its
-    // own TMA reduce-adds (box 32 x 32), so no cross-warp barrier is needed
-    uint8_t* stage = smem + L::oDQ + (warp & 3) * (kDQBufs * 4096);
+    uint8_t* stage = smem + L::oDQ + (4 + (warp & 3)) * (kDQBufs * 2048);
     int nflush = 0;
     for (int t = 0; t < nt; ++t) {
       const int i = i0 + t, st = t & 1;
       mbar_wait(&x_full[t & 3], (uint32_t)(t >> 2) & 1u);
-      const float* x = reinterpret_cast<const float*>(smem + L::oX + (t & 3) * 1024);
-      const float s_ds = x[1], rs = x[128 + r];
+      const uint32_t xs = smem_u32(smem + L::oX + (t & 3) * 1024);
+      const float s_ds = lds_f32(xs + 4), rs = lds_f32(xs + 512 + 4 * r);
       const float wk = __fmul_rn(__fmul_rn(s_ds, s_sq[i]), a.scale);  // dK carries the softmax scale (b7)
       const float wq = __fmul_rn(s_ds, sk_j);
       SAGE3_TRACE_EV(4, t, 0);
@@ -632,42 +711,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty);
       SAGE3_TRACE_EV(4, t, 2);
-      // dQ partial of (i, j): MM(dŜ, K̂_j)·s_dS·s_K + rowsum(dS)·K_m, 32 columns per TMA reduce-add
-      const uint32_t tQ = lane_base + (st ? kColS1 : kColS0);
-      const f2 wq2 = make_float2(wq, wq), rs2 = make_float2(rs, rs);
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc, ++nflush) {
-        uint8_t* buf = stage + (nflush % kDQBufs) * 4096;
-        uint32_t va[16], vb[16];
-        tmem_ld_32x32b_x16(tQ + 32 * cc, va);
-        tmem_ld_32x32b_x16(tQ + 32 * cc + 16, vb);
-        if (lane == 0) bulk_wait_read<kDQBufs - 1>();  // this warp's reduce that last read `buf` is done
-        __syncwarp();
-        tmem_ld_wait_regs(va);
-        tmem_ld_wait_regs(vb);
-        const uint32_t row = smem_u32(buf) + (r & 31) * 128;
-        auto put = [&](int hh, const uint32_t(&v)[16]) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int e = 4 * q, col = 32 * cc + 16 * hh + e;
-            const float4 km = *reinterpret_cast<const float4*>(s_km + col);
-            const f2 y0 = ffma2(i2f2b(v[e], v[e + 1]), wq2, fmul2(rs2, make_float2(km.x, km.y)));
-            const f2 y1 = ffma2(i2f2b(v[e + 2], v[e + 3]), wq2, fmul2(rs2, make_float2(km.z, km.w)));
-            sts_v4(row + (((4 * hh + q) ^ (r & 7)) * 16), __float_as_uint(y0.x), __float_as_uint(y0.y),
-                   __float_as_uint(y1.x), __float_as_uint(y1.y));
-          }
-        };
-        put(0, va);
-        put(1, vb);
-        fence_proxy_async_smem();
-        __syncwarp();
-#ifndef SAGE3_BWD_NO_DQ_REDUCE  // (experiment: measures the cost of the dQ reduce-adds; wrong dQ)
-        if (lane == 0) {
-          tma_reduce_add_2d(&tm_dqacc, buf, 32 * cc, bh * a.Np + i * 128 + (warp & 3) * 32);
-          bulk_commit();
-        }
-#endif
-      }
+      // dQ partial of (i, j): MM(dŜ, K̂_j)·s_dS·s_K + rowsum(dS)·K_m (Alg3 L10), columns [D/2, D)
+      flush_dq<D / 32>(&tm_dqacc, lane_base + (st ? kColS1 : kColS0), D / 2, stage, nflush, s_km,
+                       make_float2(wq, wq), make_float2(rs, rs), r, lane, bh * a.Np + i * 128 + (warp & 3) * 32,
+                       a.dqacc + ((int64_t)bh * a.Np + i * 128 + r) * D);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sb_empty[st]);
@@ -834,11 +881,11 @@ cudaError_t launch_bwd_d(const I8BwdArgs& a, cudaStream_t stream) {
   const uint64_t rows = (uint64_t)BH * a.Np;
   CUtensorMap tq, tk, tdq8, tv, tdo, tacc;
   const cuuint64_t adims[2] = {(cuuint64_t)D, rows}, astr[1] = {(cuuint64_t)D * 4};
-  const cuuint32_t abox[2] = {32, 32};
+  const cuuint32_t abox[2] = {16, 32};
   if (!map_i8(&tq, a.q8, D, rows) || !map_i8(&tk, a.k8, D, rows) || !map_i8(&tdq8, a.do8, D, rows) ||
       !map_16(&tv, a.v, a.B, a.H, a.N, D, a.v_sb, a.v_sh, a.v_sn) ||
       !map_16(&tdo, a.dout, a.B, a.H, a.N, D, a.do_sb, a.do_sh, a.do_sn) ||
-      !encode_map(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a.dqacc, adims, astr, abox, CU_TENSOR_MAP_SWIZZLE_128B))
+      !encode_map(&tacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a.dqacc, adims, astr, abox, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(a.dqacc, 0, rows * D * sizeof(float), stream);
   if (e != cudaSuccess) return e;

@@ -34,6 +34,7 @@ nt = min(N // 128, 128)
 names = {1: ["wait_q+S", "A+redA", "wait_dP/sp", "B", "redB", "wait_sds", "C"],
          2: ["S(t+1)", "dV(t)", "dKQ(t)", "dP(t+1)"], 3: ["wait_qe", "wait_doe", "wait_dq8e"],
          4: ["wait_kq", "dKp", "dQflush"], 5: ["wait_dvp", "dVacc"]}
+sub = {4: [(2, 4, "flush0: ld+wait"), (4, 5, "flush0: compute+sts"), (5, 6, "flush0: fence"), (6, 3, "rest")]}
 for cta in range(2):
     t = buf[cta].astype(np.int64)
     js = range(4, nt - 4)
@@ -44,6 +45,9 @@ for cta in range(2):
             v = [t[role, j, k + 1] - t[role, j, k] for j in js if t[role, j, k + 1] and t[role, j, k]]
             segs.append(f"{nm[k]} {np.mean(v):6.0f}" if v else f"{nm[k]} -")
         print(f"  role {role}: " + " | ".join(segs))
+        for k0, k1, nm2 in sub.get(role, []):
+            v = [t[role, j, k1] - t[role, j, k0] for j in js if t[role, j, k1] and t[role, j, k0]]
+            print(f"      {nm2} {np.mean(v):6.0f}")
     # cross-role latencies
     lat = lambda a, b: np.mean([t[b[0], j + b[2], b[1]] - t[a[0], j, a[1]] for j in js])  # noqa: E731
     print(f"  ds_full(t) -> MMA dKQ issued {lat((1, 7, 0), (2, 3, 0)):6.0f};  dKQ issued -> WG3 kq {lat((2, 3, 0), (4, 1, 0)):6.0f};"
