@@ -88,3 +88,25 @@ def test_binding_refuses_missing_library(monkeypatch, tmp_path):
     monkeypatch.setattr(s3, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(s3.Sage3Error):
         s3.load()
+
+
+def test_int8_bwd_host_checks(lib):
+    """sage3_int8_attn_bwd: workspace size query and host-side rejections (no device needed)."""
+    B, H, N, d = 2, 3, 300, 64
+    Np = 384
+    al = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    want = al(B * H * Np * d) + al(B * H * (Np // 128) * 4) + 2 * al(B * H * Np * 4) + al(B * H * Np * d * 4)
+    assert s3.sage3_int8_bwd_workspace_bytes(B, H, N, d) == want
+    assert s3.sage3_int8_bwd_workspace_bytes(1, 1, 128, 96) == 0
+    t = s3.Tensor4(1 << 20, 0, 0, 64)
+    z = s3.Tensor4(None, 0, 0, 0)
+    q = s3.INT8QKVStruct(1, 1, 128, 64, 128)
+    args = lambda qq, v, lse, gdt, ws, wsb: lib.sage3_int8_attn_bwd(  # noqa: E731
+        qq, v, t, s3.SAGE3_FP32, t, s3.SAGE3_BF16, lse, 0, 0.0, t, t, t, gdt, ws, wsb, None)
+    assert args(None, t, 16, s3.SAGE3_FP32, 1 << 20, 1 << 30) == s3.SAGE3_ERR_INVALID_ARG  # null qkv
+    assert args(ctypes.byref(q), t, 16, s3.SAGE3_FP32, 1 << 20, 1 << 30) == s3.SAGE3_ERR_INVALID_ARG  # null codes
+    q.q = q.k = q.s_q = q.s_k = q.k_mean = 1 << 20
+    assert args(ctypes.byref(q), z, 16, s3.SAGE3_FP32, 1 << 20, 1 << 30) == s3.SAGE3_ERR_INVALID_ARG  # null v
+    assert args(ctypes.byref(q), t, None, s3.SAGE3_FP32, 1 << 20, 1 << 30) == s3.SAGE3_ERR_INVALID_ARG  # null lse
+    assert args(ctypes.byref(q), t, 16, 7, 1 << 20, 1 << 30) == s3.SAGE3_ERR_UNSUPPORTED  # gradient dtype
+    assert args(ctypes.byref(q), t, 16, s3.SAGE3_FP32, 1 << 20, 16) == s3.SAGE3_ERR_WORKSPACE

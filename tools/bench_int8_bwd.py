@@ -15,7 +15,7 @@ import synth  # noqa: E402
 
 
 def main():
-    H, d = 32, 128
+    H, d = 32, int(os.environ.get("SAGE3_D", "128"))
     Ns = [int(x) for x in sys.argv[1:]] or [4096, 16384, 32768]
     for N in Ns:
         Q, K, V = synth.make_qkv(1, H, N, d, seed=0, dtype=torch.bfloat16, device="cuda")
