@@ -26,6 +26,9 @@ namespace {
 
 using namespace ptx;
 
+#ifndef SAGE3_I8_ROLLED
+#define SAGE3_I8_ROLLED 1
+#endif
 constexpr int kIKStages = 3, kIVStages = 3, kIPBufs = 3, kIXSlots = 8, kISBufs = 3;
 constexpr int kIThreads = 512;
 constexpr uint32_t kIRegWG0 = 32, kIRegSoftmax = 144, kIRegCorrection = 192;
@@ -291,6 +294,18 @@ __global__ void __launch_bounds__(kIThreads, 1)
         sts_v4(sP + (((2 * cc) ^ (r & 7)) * 16), w[0], w[1], w[2], w[3]);
         sts_v4(sP + (((2 * cc + 1) ^ (r & 7)) * 16), w[4], w[5], w[6], w[7]);
       };
+#if SAGE3_I8_ROLLED
+#pragma unroll 1  // rolled: smaller per-role code (the warp roles share each sub-partition's i-cache)
+      for (int cc = 0; cc < 4; cc += 2) {
+        uint32_t va[32], vb[32];
+        tmem_ld_32x32b_x32(s_addr + 32 * cc, va);
+        tmem_ld_32x32b_x32(s_addr + 32 * cc + 32, vb);
+        tmem_ld_wait_regs(va);
+        tmem_ld_wait_regs(vb);
+        chunk(cc, va);
+        chunk(cc + 1, vb);
+      }
+#else
       {
         uint32_t va[32], vb[32];
         tmem_ld_32x32b_x32(s_addr, va);
@@ -306,6 +321,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         tmem_ld_wait_regs(vb);
         chunk(3, vb);
       }
+#endif
       const int slot = j % kIXSlots;
       sts_f32(xchg_s + slot * 1024, tmax);
       sts_f32(xchg_s + slot * 1024 + 512, rowsum);
