@@ -1,5 +1,5 @@
 """Small end-to-end cases for compute-sanitizer (SURVEY §4 layer 7): quantize + attention (d 64/128, causal
-and not, ragged N, smoothing Q, MXFP4, direct and lazy P, SageBwd INT8 forward) through the C ABI, plus the
+and not, ragged N, smoothing Q, MXFP4, direct and lazy P, SageBwd INT8 forward and backward) through the C ABI, plus the
 host-buffer path.
   compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_case.py"""
 import os
@@ -21,7 +21,10 @@ for d in (64, 128):
             s3.attention(Q, K, V, causal=causal, p_quant="direct")
             s3.attention(Q, K, V, causal=causal, p_quant="lazy")
             s3.attention(Q, K, V, causal=causal, fmt="mxfp4", p_quant="lazy")
-            s3.sage3_int8_attn_fwd(s3.sage3_int8_quantize_qkv(Q, K, V), causal=causal)
+            qkv8 = s3.sage3_int8_quantize_qkv(Q, K, V)
+            lse = torch.empty(1, 1, N, dtype=torch.float32, device="cuda")
+            O8 = s3.sage3_int8_attn_fwd(qkv8, causal=causal, lse=lse)
+            s3.sage3_int8_attn_bwd(qkv8, V, O8, torch.randn_like(Q), lse, causal=causal)
             torch.cuda.synchronize()
 Q, K, V = synth.make_qkv(1, 2, 300, 128, seed=1, dtype=torch.bfloat16, device="cpu")
 qh, kh, vh = (x.pin_memory() for x in (Q, K, V))
