@@ -108,7 +108,8 @@ struct Layout {
 template <int D, bool kSQ, bool kMX, bool kDirect>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const AttnArgs a) {
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                    const AttnArgs a) {
   using L = Layout<D, kMX>;
   extern __shared__ uint8_t smem_raw[];
   // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int qt = n_qt - 1 - (int)(unit % n_qt);
   const int nkv = a.causal ? qt + 1 : n_qt;
 
+  SAGE3_TRACE_EV(0, 127, 0);  // CTA start (thread 0)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < kKStages; ++s) {
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  SAGE3_TRACE_EV(0, 127, 1);  // prologue done
   const uint32_t tbase = *tmem_slot;
   const int wg = warp >> 2;
 
@@ -587,42 +590,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Alg1 L13: O_i = diag(l)^-1 O_i
     if (a.lse != nullptr && q_row < a.N) a.lse[(int64_t)bh * a.N + q_row] = m * a.scale + logf(l);
     const float inv_l = 1.0f / l;
-    if (q_row < a.N) {
-      const int b = bh / a.H, h = bh % a.H;
-      const f2 il{inv_l, inv_l};
+    const f2 il{inv_l, inv_l};
 #pragma unroll
-      for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
-      if (a.o_dtype == 2) {
-        float* dst = reinterpret_cast<float*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
-#pragma unroll
-        for (int c = 0; c < D / 2; c += 2)
-          *reinterpret_cast<float4*>(dst + 2 * c) = make_float4(o[c].x, o[c].y, o[c + 1].x, o[c + 1].y);
-      } else if (a.o_dtype == 1) {
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
-#pragma unroll
-        for (int c = 0; c < D / 2; c += 4) {
-          uint4 u;
-          __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(o[c + i].x, o[c + i].y);
-          *reinterpret_cast<uint4*>(dst + 2 * c) = u;
-        }
-      } else {
-        __half* dst = reinterpret_cast<__half*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
-#pragma unroll
-        for (int c = 0; c < D / 2; c += 4) {
-          uint4 u;
-          __half2* p = reinterpret_cast<__half2*>(&u);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) p[i] = __floats2half2_rn(o[c + i].x, o[c + i].y);
-          *reinterpret_cast<uint4*>(dst + 2 * c) = u;
-        }
-      }
-    }
+    for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
+    // coalesced store: rows -> smem (the K/V rings, idle once the last PV MMA has completed) -> TMA
+    uint8_t* stage = smem + L::oK;
+    stage_o_row<D>(stage, r, a.o_dtype, o);
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 128) store_o_tile<D>(&tm_o, stage, a.o_dtype, qt * 128, bh % a.H, bh / a.H);
   }
-
+  SAGE3_TRACE_EV(4, 127, 2);  // correction: epilogue stores issued (thread 128)
   tc_fence_before();
   __syncthreads();
+  SAGE3_TRACE_EV(0, 127, 3);  // all roles done
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
@@ -642,14 +623,15 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     attr_done[dev] = true;
   }
   const int BH = a.B * a.H;
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, to;
   if (!make_map(&tq, a.q_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
       !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
-      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D))
+      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D) ||
+      !make_map_o(&to, a.o, a.o_dtype, a.B, a.H, a.N, D, a.o_sb, a.o_sh, a.o_sn))
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_fwd_kernel<D, kSQ, kMX, kDirect><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
+  attn_fwd_kernel<D, kSQ, kMX, kDirect><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
   return cudaGetLastError();
 }
 

@@ -8,6 +8,9 @@
 #include <cstdint>
 #include <mutex>
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "sm100.cuh"
 
 namespace sage3 {
@@ -141,6 +144,65 @@ __device__ unsigned long long g_trace[2][8][128][8];
   } while (0)
 #endif
 
+// ---------------------------------------------------------------- coalesced O epilogue (TMA store)
+// The epilogue's per-thread row stores (one query row per thread, rows 2·d bytes apart) cost ~32 L1 wavefronts
+// per warp instruction; instead each thread writes its row into smem in the SWIZZLE_128B box layout and one
+// thread issues TMA tensor stores of [128 rows][128 B] boxes (rows >= N are clipped by the tensor map).
+__device__ __forceinline__ void tma_store_4d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1, int32_t c2,
+                                             int32_t c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_group_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_group_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// Row r of the O tile (D values o, already divided by l) -> smem staging at `stage` (1024-aligned, D·esize·128
+// bytes): box b = 128-byte column slice b, [128 rows][128 B], 16-byte chunk q of row r at (q ^ (r & 7)).
+template <int D>
+__device__ __forceinline__ void stage_o_row(uint8_t* stage, int r, int dt, const float2* o) {
+  const uint32_t base = smem_u32(stage) + r * 128;
+  if (dt == 2) {  // fp32: 32 values per box
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) {  // chunk c = values 4c..4c+3
+      const int bx = c >> 3, q = c & 7;
+      sts_v4(base + bx * 16384 + ((q ^ (r & 7)) * 16), __float_as_uint(o[2 * c].x), __float_as_uint(o[2 * c].y),
+             __float_as_uint(o[2 * c + 1].x), __float_as_uint(o[2 * c + 1].y));
+    }
+  } else {  // 16-bit: 64 values per box
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {  // chunk c = values 8c..8c+7
+      const int bx = c >> 3, q = c & 7;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 v = o[4 * c + e];
+        if (dt == 1) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v.x, v.y);
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        } else {
+          __half2 h2 = __floats2half2_rn(v.x, v.y);
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+      }
+      sts_v4(base + bx * 16384 + ((q ^ (r & 7)) * 16), w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+// The staged tile -> O[b][h][q0 .. q0+128)[0 .. D) (one thread; waits until smem has been read).
+template <int D>
+__device__ __forceinline__ void store_o_tile(const void* tm_o, const uint8_t* stage, int dt, int q0, int h, int b) {
+  const int boxes = D * (dt == 2 ? 4 : 2) / 128, per = dt == 2 ? 32 : 64;
+  for (int bx = 0; bx < boxes; ++bx) tma_store_4d(tm_o, stage + bx * 16384, bx * per, q0, h, b);
+  bulk_group_commit();
+  bulk_group_wait_read0();
+}
+
 // ------------------------------------------------------------------------------------------- host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -168,6 +230,24 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t row
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// O [B][H][N][D] (element strides, d-stride 1) in sage3_dtype dt: 4-D map with 128-byte x 128-row boxes,
+// SWIZZLE_128B (the layout stage_o_row writes).
+bool make_map_o(CUtensorMap* m, const void* base, int dt, int B, int H, int N, int D, int64_t sb, int64_t sh,
+                int64_t sn) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  const int es = dt == 2 ? 4 : 2;
+  if (H == 1) sh = sn * N;
+  if (B == 1) sb = sh * H;
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)sn * es, (cuuint64_t)sh * es, (cuuint64_t)sb * es};
+  cuuint32_t box[4] = {(cuuint32_t)(128 / es), 128, 1, 1};
+  cuuint32_t ones[4] = {1, 1, 1, 1};
+  return enc(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base),
+             dims, strides, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
