@@ -194,6 +194,33 @@ __device__ __forceinline__ void stage_o_row(uint8_t* stage, int r, int dt, const
     }
   }
 }
+// Columns [32c, 32c + 32) of row r (fp32 values f, already divided by l) -> the same staging layout.
+__device__ __forceinline__ void stage_o_cols32(uint8_t* stage, int r, int dt, int c, const float* f) {
+  const uint32_t base = smem_u32(stage) + r * 128;
+  if (dt == 2) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)  // chunk 8c + k: box c, position k
+      sts_v4(base + c * 16384 + ((k ^ (r & 7)) * 16), __float_as_uint(f[4 * k]), __float_as_uint(f[4 * k + 1]),
+             __float_as_uint(f[4 * k + 2]), __float_as_uint(f[4 * k + 3]));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // chunk 4c + k
+      const int ch = 4 * c + k, bx = ch >> 3, q = ch & 7;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (dt == 1) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(f[8 * k + 2 * e], f[8 * k + 2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        } else {
+          __half2 h2 = __floats2half2_rn(f[8 * k + 2 * e], f[8 * k + 2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+      }
+      sts_v4(base + bx * 16384 + ((q ^ (r & 7)) * 16), w[0], w[1], w[2], w[3]);
+    }
+  }
+}
 // The staged tile -> O[b][h][q0 .. q0+128)[0 .. D) (one thread; waits until smem has been read).
 template <int D>
 __device__ __forceinline__ void store_o_tile(const void* tm_o, const uint8_t* stage, int dt, int q0, int h, int b) {

@@ -78,7 +78,8 @@ struct I8Layout {
 template <int D>
 __global__ void __launch_bounds__(kIThreads, 1)
     attn_i8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, const I8AttnArgs a) {
+                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                   const I8AttnArgs a) {
   using L = I8Layout<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -387,38 +388,14 @@ __global__ void __launch_bounds__(kIThreads, 1)
     }
     if (a.lse != nullptr && q_row < a.N) a.lse[(int64_t)bh * a.N + q_row] = mref * a.scale + logf(l);
     const float inv_l = 1.0f / l;
-    if (q_row < a.N) {
-      const int b = bh / a.H, h = bh % a.H;
-      const f2 il{inv_l, inv_l};
+    const f2 il{inv_l, inv_l};
 #pragma unroll
-      for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
-      if (a.o_dtype == 2) {
-        float* dst = reinterpret_cast<float*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
-#pragma unroll
-        for (int c = 0; c < D / 2; c += 2)
-          *reinterpret_cast<float4*>(dst + 2 * c) = make_float4(o[c].x, o[c].y, o[c + 1].x, o[c + 1].y);
-      } else if (a.o_dtype == 1) {
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
-#pragma unroll
-        for (int c = 0; c < D / 2; c += 4) {
-          uint4 u;
-          __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(o[c + i].x, o[c + i].y);
-          *reinterpret_cast<uint4*>(dst + 2 * c) = u;
-        }
-      } else {
-        __half* dst = reinterpret_cast<__half*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn;
-#pragma unroll
-        for (int c = 0; c < D / 2; c += 4) {
-          uint4 u;
-          __half2* p = reinterpret_cast<__half2*>(&u);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) p[i] = __floats2half2_rn(o[c + i].x, o[c + i].y);
-          *reinterpret_cast<uint4*>(dst + 2 * c) = u;
-        }
-      }
-    }
+    for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
+    uint8_t* stage = smem + L::oK;  // coalesced store through smem + TMA (as attn.cu)
+    stage_o_row<D>(stage, r, a.o_dtype, o);
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 128) store_o_tile<D>(&tm_o, stage, a.o_dtype, qt * 128, bh % a.H, bh / a.H);
   }
 
   tc_fence_before();
@@ -456,12 +433,13 @@ cudaError_t launch_i8_d(const I8AttnArgs& a, cudaStream_t stream) {
     attr_done[dev] = true;
   }
   const int BH = a.B * a.H;
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, to;
   if (!make_map_i8(&tq, a.q8, D, (uint64_t)BH * a.Np, D, 128) || !make_map_i8(&tk, a.k8, D, (uint64_t)BH * a.Np, D, 128) ||
-      !make_map_i8(&tv, a.vt8, (uint64_t)a.Np, (uint64_t)BH * D, 128, D))
+      !make_map_i8(&tv, a.vt8, (uint64_t)a.Np, (uint64_t)BH * D, 128, D) ||
+      !make_map_o(&to, a.o, a.o_dtype, a.B, a.H, a.N, D, a.o_sb, a.o_sh, a.o_sn))
     return cudaErrorInvalidValue;
   const int64_t units = (int64_t)BH * (a.Np / 128);
-  attn_i8_kernel<D><<<(unsigned)units, kIThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
+  attn_i8_kernel<D><<<(unsigned)units, kIThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
   return cudaGetLastError();
 }
 

@@ -116,7 +116,8 @@ struct LazyLayout {
 template <int D, bool kMX>
 __global__ void __launch_bounds__(kLThreads, 1)
     attn_lazy_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                     const __grid_constant__ CUtensorMap tm_v, const AttnArgs a) {
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                     const AttnArgs a) {
   using L = LazyLayout<D, kMX>;
   using C = LazyCfg<kMX>;
   extern __shared__ uint8_t smem_raw[];
@@ -527,44 +528,21 @@ __global__ void __launch_bounds__(kLThreads, 1)
     tc_fence_after();
     if (a.lse != nullptr && q_row < a.N) a.lse[(int64_t)bh * a.N + q_row] = rprev * a.scale + logf(l) - kLnTop;
     const float inv_l = 1.0f / l;
-    const int b = bh / a.H, h = bh % a.H;
+    // coalesced store through smem (the K/V rings are idle after the last PV MMA) and TMA (as attn.cu)
+    uint8_t* stage = smem + L::oK;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t o[32];
       tmem_ld_32x32b_x32(lane_o + 32 * c, o);
       tmem_ld_wait_regs(o);
-      if (q_row < a.N) {
-        float* f = reinterpret_cast<float*>(o);
+      float* f = reinterpret_cast<float*>(o);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] *= inv_l;
-        if (a.o_dtype == 2) {
-          float* dst = reinterpret_cast<float*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn + 32 * c;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]);
-        } else if (a.o_dtype == 1) {
-          __nv_bfloat16* dst =
-              reinterpret_cast<__nv_bfloat16*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn + 32 * c;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 u;
-            __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) p[k] = __floats2bfloat162_rn(f[i + 2 * k], f[i + 2 * k + 1]);
-            *reinterpret_cast<uint4*>(dst + i) = u;
-          }
-        } else {
-          __half* dst = reinterpret_cast<__half*>(a.o) + b * a.o_sb + h * a.o_sh + (int64_t)q_row * a.o_sn + 32 * c;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 u;
-            __half2* p = reinterpret_cast<__half2*>(&u);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) p[k] = __floats2half2_rn(f[i + 2 * k], f[i + 2 * k + 1]);
-            *reinterpret_cast<uint4*>(dst + i) = u;
-          }
-        }
-      }
+      for (int i = 0; i < 32; ++i) f[i] *= inv_l;
+      stage_o_cols32(stage, r, a.o_dtype, c, f);
     }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 128) store_o_tile<D>(&tm_o, stage, a.o_dtype, qt * 128, bh % a.H, bh / a.H);
   }
 
   tc_fence_before();
@@ -589,13 +567,15 @@ cudaError_t launch_lazy_d(const AttnArgs& a, cudaStream_t stream) {
   }
   const int BH = a.B * a.H;
   CUtensorMap tq, tk, tv;
+  CUtensorMap to;
   if (!make_map(&tq, a.q_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
       !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
-      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D))
+      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D) ||
+      !make_map_o(&to, a.o, a.o_dtype, a.B, a.H, a.N, D, a.o_sb, a.o_sh, a.o_sn))
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_lazy_kernel<D, kMX><<<(unsigned)units, kLThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, a);
+  attn_lazy_kernel<D, kMX><<<(unsigned)units, kLThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
   return cudaGetLastError();
 }
 
