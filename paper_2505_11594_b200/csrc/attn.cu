@@ -587,17 +587,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       SAGE3_TRACE_EV(4, j, 3);
     }
     const float m = mref;
+    SAGE3_TRACE_EV(4, 126, 0);
     // Alg1 L13: O_i = diag(l)^-1 O_i
     if (a.lse != nullptr && q_row < a.N) a.lse[(int64_t)bh * a.N + q_row] = m * a.scale + logf(l);
     const float inv_l = 1.0f / l;
     const f2 il{inv_l, inv_l};
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
+    SAGE3_TRACE_EV(4, 126, 1);
     // coalesced store: rows -> smem (the K/V rings, idle once the last PV MMA has completed) -> TMA
     uint8_t* stage = smem + L::oK;
     stage_o_row<D>(stage, r, a.o_dtype, o);
+    SAGE3_TRACE_EV(4, 126, 2);
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
+    SAGE3_TRACE_EV(4, 126, 3);
     if (threadIdx.x == 128) store_o_tile<D>(&tm_o, stage, a.o_dtype, qt * 128, bh % a.H, bh / a.H);
   }
   SAGE3_TRACE_EV(4, 127, 2);  // correction: epilogue stores issued (thread 128)

@@ -145,7 +145,7 @@ __device__ __forceinline__ void store_row(void* base, int64_t sb, int64_t sh, in
 // One warp's share of a dQ partial: columns [c0, c0 + 16·NCH) of its 32 rows (TMEM lanes), scaled
 // y = int·w_q + rowsum(dS)·K_m, staged in smem ([32 rows][16 fp32], SWIZZLE_64B, kDQBufs buffers per warp)
 // and added into the fp32 dQ accumulator by this warp's own TMA reduce-adds (box 16 x 32).
-__device__ __forceinline__ void red_add_v4(float* gaddr, f2 a, f2 b) {
+__device__ __forceinline__ __attribute__((unused)) void red_add_v4(float* gaddr, f2 a, f2 b) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gaddr), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y)
                : "memory");
 }

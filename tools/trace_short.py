@@ -26,7 +26,7 @@ buf = np.zeros((2, 8, 128, 8), np.uint64)
 L = s3.load()
 L.sage3_debug_trace_copy.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert L.sage3_debug_trace_copy(buf.ctypes.data, buf.nbytes) == 0
-nkv = N // 128
+nkv = min(N // 128, 128)
 for cta in range(2):
     t = buf[cta].astype(np.int64)
     t0 = t[0, 127, 0]
@@ -36,5 +36,6 @@ for cta in range(2):
           f" PV0 issued {r(t[6,0,3])}; correction tile0 done {r(t[4,0,3])}")
     print(f"  last tile: S issued {r(t[5,nkv-1,3])}; P ready {r(t[1 + (nkv-1)%2, nkv-1, 4])}; correction done {r(t[4,nkv-1,3])};"
           f" epilogue stores {r(t[4,127,2])}; all done {r(t[0,127,3])}")
+    print(f"  epilogue: loop exit {r(t[4,126,0])}, normalized {r(t[4,126,1])}, staged {r(t[4,126,2])}, barrier {r(t[4,126,3])}")
     steady = (t[4, nkv - 1, 3] - t[4, 0, 3]) / max(nkv - 1, 1)
     print(f"  per-tile (correction done spacing) {steady:.0f}")
