@@ -43,6 +43,9 @@ namespace {
 
 using namespace ptx;
 
+#ifndef SAGE3_FUSED_P2
+#define SAGE3_FUSED_P2 0
+#endif
 constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
@@ -488,6 +491,51 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 16-byte chunk c = keys [32c, 32c+32) of row r, SWIZZLE_64B (chunk ^= (row>>1)&3)
         sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
       };
+#if SAGE3_FUSED_P2
+      // exps of chunk c and the finish of chunk c-1 fused quarter by quarter (4 pairs of exps, then one E2M1
+      // word and one partial row sum of the previous chunk), spreading the MUFU issue between FMA/ALU work;
+      // the same operations in the same tree order as exps + finish (bitwise identical results).
+      auto step = [&](int c, const uint32_t(&v)[32], f2(&y)[16], int cp, const f2(&yp)[16]) {
+        const float nA = c == 1 ? nbb[2] : c == 2 ? nbb[4] : nbb[6];
+        const float nB = c == 1 ? nbb[3] : c == 2 ? nbb[5] : nbb[7];
+        const float sA = cp == 0 ? sdec[0] : cp == 1 ? sdec[2] : sdec[4];
+        const float sB = cp == 0 ? sdec[1] : cp == 1 ? sdec[3] : sdec[5];
+        uint32_t w[4];
+        f2 qs[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int i = 4 * q; i < 4 * q + 4; ++i) {
+            const float nbh = i < 8 ? nA : nB;
+            const f2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2,
+                               make_float2(nbh, nbh));
+            y[i] = ((kPolyMask >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          }
+          const f2* yy = yp + 4 * q;
+          qs[q] = fadd2(fadd2(yy[0], yy[1]), fadd2(yy[2], yy[3]));
+          w[q] = cvt_e2m1x8(yy[0].x, yy[0].y, yy[1].x, yy[1].y, yy[2].x, yy[2].y, yy[3].x, yy[3].y);
+        }
+        const f2 syA = fadd2(qs[0], qs[1]), syB = fadd2(qs[2], qs[3]);
+        rowsum = fmaf(sA, syA.x + syA.y, rowsum);
+        rowsum = fmaf(sB, syB.x + syB.y, rowsum);
+        sts_v4(sP + ((cp ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
+      };
+      {
+        f2 ya[16], yb[16];
+        tmem_ld_wait_regs(va);
+        tmem_ld_32x32b_x32(s_addr + 32, vb);
+        exps(0, va, ya);
+        tmem_ld_wait_regs(vb);
+        tmem_ld_32x32b_x32(s_addr + 64, va);
+        step(1, vb, yb, 0, ya);
+        tmem_ld_wait_regs(va);
+        tmem_ld_32x32b_x32(s_addr + 96, vb);
+        step(2, va, ya, 1, yb);
+        tmem_ld_wait_regs(vb);
+        step(3, vb, yb, 2, ya);
+        finish(3, yb);
+      }
+#else
       {
         f2 ya[16], yb[16];
         tmem_ld_wait_regs(va);
@@ -508,6 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         finish(2, ya);
         finish(3, yb);
       }
+#endif
       sts_u32(sPSF, scw[0]);
       if constexpr (!kMX) sts_u32(sPSF + 512, scw[1]);
       if constexpr (!kDirect) sts_f32(xchg_s + slot * 1024, eref);
