@@ -349,9 +349,12 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
         const uint32_t sc2 = cvt_e4m3x2(__fmul_rn(a0, kOneSixth), __fmul_rn(a1, kOneSixth));
         const uint32_t sc0 = sc2 & 0xFFu, sc1 = (sc2 >> 8) & 0xFFu;
         const float r0 = s_rcp[sc0], r1 = s_rcp[sc1];
-        *reinterpret_cast<uint2*>(vcode + c * 64 + tb * 8) =
+        // 8-byte group tb of channel rows c, c+1 at position tb ^ ((c >> 1) & 7): the 32 threads of a warp
+        // (consecutive channel pairs, same tb) spread over 8 positions instead of one bank (was 32-way)
+        const int pos = (tb ^ ((c >> 1) & 7)) * 8;
+        *reinterpret_cast<uint2*>(vcode + c * 64 + pos) =
             sc0 ? make_uint2(codes8(x0, r0), codes8(x0 + 8, r0)) : make_uint2(0u, 0u);
-        *reinterpret_cast<uint2*>(vcode + (c + 1) * 64 + tb * 8) =
+        *reinterpret_cast<uint2*>(vcode + (c + 1) * 64 + pos) =
             sc1 ? make_uint2(codes8(x1, r1), codes8(x1 + 8, r1)) : make_uint2(0u, 0u);
         const int base = (tb >> 2) * 512 + ((c >> 5) & 3) * 4 + (tb & 3);
         sfs[base + (c & 31) * 16] = (uint8_t)sc0;
@@ -361,10 +364,18 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
       __syncwarp();
       if ((t & 31) == 0) mbar_arrive(&empty[s]);
       consumer_bar();
-      for (int i = t; i < D * 4; i += 256) {
-        const int c = i >> 2, q = i & 3;
-        *reinterpret_cast<uint4*>(va.v_data + ((int64_t)bh * D + c) * (qa.Np >> 1) + chunk * 64 + q * 16) =
-            *reinterpret_cast<const uint4*>(vcode + c * 64 + q * 16);
+      if constexpr (kMX) {
+        for (int i = t; i < D * 4; i += 256) {
+          const int c = i >> 2, q = i & 3;
+          *reinterpret_cast<uint4*>(va.v_data + ((int64_t)bh * D + c) * (qa.Np >> 1) + chunk * 64 + q * 16) =
+              *reinterpret_cast<const uint4*>(vcode + c * 64 + q * 16);
+        }
+      } else {  // un-swizzle: 8 threads per channel row, 8 bytes each (coalesced 64-byte rows)
+        for (int i = t; i < D * 8; i += 256) {
+          const int c = i >> 3, g = i & 7;
+          *reinterpret_cast<uint2*>(va.v_data + ((int64_t)bh * D + c) * (qa.Np >> 1) + chunk * 64 + g * 8) =
+              *reinterpret_cast<const uint2*>(vcode + c * 64 + ((g ^ ((c >> 1) & 7)) * 8));
+        }
       }
       constexpr int kSFv = kMX ? 512 : 1024;  // SF bytes of one 128-token chunk (128 channel rows)
       uint8_t* sf_dst = va.v_sf + ((int64_t)bh * nch + chunk) * kSFv;
