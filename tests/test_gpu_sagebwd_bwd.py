@@ -49,7 +49,8 @@ def _check(got, ref, what):
 
 
 @pytest.mark.parametrize("N,d,causal", [(128, 64, False), (128, 128, True), (300, 128, False), (300, 64, True),
-                                        (1000, 128, True), (1000, 64, False), (640, 128, False)])
+                                        (1000, 128, True), (1000, 64, False), (640, 128, False), (2500, 64, True),
+                                        (2100, 128, False)])
 def test_int8_bwd_parity(N, d, causal):
     B, H = 1, 2
     _, _, V, dO, O, L, qkv, refs, scale = _case(B, H, N, d, causal, seed=N + d + int(causal))
