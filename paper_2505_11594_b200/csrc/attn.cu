@@ -43,6 +43,12 @@ namespace {
 
 using namespace ptx;
 
+#ifndef SAGE3_EARLY_TMA
+#define SAGE3_EARLY_TMA 0
+#endif
+#ifndef SAGE3_EARLY_K
+#define SAGE3_EARLY_K 1  // K tiles requested in the prologue (<= kKStages)
+#endif
 #ifndef SAGE3_FUSED_P2
 #define SAGE3_FUSED_P2 0
 #endif
@@ -175,11 +181,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ds_empty[s], 4);  // one arrival per softmax warp of the tile's warpgroup
     }
     fence_mbar_init();
-  }
-  if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_q);
     prefetch_tmap(&tm_k);
     prefetch_tmap(&tm_v);
+#if SAGE3_EARLY_TMA
+    // the Q tile and the first K tiles are requested before the prologue's __syncthreads (the rings are empty
+    // and the barriers initialised by this thread), overlapping their latency with TMEM allocation and setup
+    const int row_q = bh * a.Np + qt * 128;
+    mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
+    tma_load_2d(smem + L::oQ, &tm_q, q_full, 0, row_q);
+    bulk_load(smem + L::oQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
+    for (int j = 0; j < nkv && j < SAGE3_EARLY_K; ++j) {
+      const int row_k = bh * a.Np + j * 128;
+      mbar_arrive_expect_tx(&k_full[j], L::kKBytes + L::kQKSF);
+      tma_load_2d(smem + L::oK + j * L::kKSlot, &tm_k, &k_full[j], 0, row_k);
+      bulk_load(smem + L::oKSF + j * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF, &k_full[j]);
+    }
+#endif
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
   if (threadIdx.x >= 128 && threadIdx.x < 256) {  // exact reciprocal of every E4M3 scale; 0 for s = 0
@@ -202,11 +220,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer: Q, K
       if (elect_one()) {
+#if SAGE3_EARLY_TMA
+        for (int j = SAGE3_EARLY_K; j < nkv; ++j) {  // Q and the first SAGE3_EARLY_K K tiles: issued in the prologue
+#else
         const int row_q = bh * a.Np + qt * 128;
         mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
         tma_load_2d(sQ, &tm_q, q_full, 0, row_q);
         bulk_load(sQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
         for (int j = 0; j < nkv; ++j) {
+#endif
           const int st = j % kKStages;
           const int row_k = bh * a.Np + j * 128;
           mbar_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
