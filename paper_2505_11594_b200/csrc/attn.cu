@@ -44,8 +44,9 @@ namespace {
 using namespace ptx;
 
 #ifndef SAGE3_EARLY_TMA
-#define SAGE3_EARLY_TMA 0
+#define SAGE3_EARLY_TMA 1  // 0: never launch the kEarly instantiation
 #endif
+constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly instantiation
 #ifndef SAGE3_EARLY_K
 #define SAGE3_EARLY_K 1  // K tiles requested in the prologue (<= kKStages)
 #endif
@@ -114,7 +115,7 @@ struct Layout {
 // RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
 // of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
 // warpgroups are no longer independent in this mode.
-template <int D, bool kSQ, bool kMX, bool kDirect>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -184,9 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tm_q);
     prefetch_tmap(&tm_k);
     prefetch_tmap(&tm_v);
-#if SAGE3_EARLY_TMA
-    // the Q tile and the first K tiles are requested before the prologue's __syncthreads (the rings are empty
-    // and the barriers initialised by this thread), overlapping their latency with TMEM allocation and setup
+    // kEarly: the Q tile and the first K tiles are requested before the prologue's __syncthreads (the rings
+    // are empty and the barriers initialised by this thread), overlapping their latency with TMEM allocation
+    // and setup.  A separate instantiation, launched for long sequences only (same-box A/B: +0.8% at N = 8K-32K,
+    // while the same code path costs 2-4% at N = 1K).
+    if constexpr (kEarly) {
     const int row_q = bh * a.Np + qt * 128;
     mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
     tma_load_2d(smem + L::oQ, &tm_q, q_full, 0, row_q);
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_2d(smem + L::oK + j * L::kKSlot, &tm_k, &k_full[j], 0, row_k);
       bulk_load(smem + L::oKSF + j * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF, &k_full[j]);
     }
-#endif
+    }
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
   if (threadIdx.x >= 128 && threadIdx.x < 256) {  // exact reciprocal of every E4M3 scale; 0 for s = 0
@@ -220,15 +223,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer: Q, K
       if (elect_one()) {
-#if SAGE3_EARLY_TMA
-        for (int j = SAGE3_EARLY_K; j < nkv; ++j) {  // Q and the first SAGE3_EARLY_K K tiles: issued in the prologue
-#else
-        const int row_q = bh * a.Np + qt * 128;
-        mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
-        tma_load_2d(sQ, &tm_q, q_full, 0, row_q);
-        bulk_load(sQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
-        for (int j = 0; j < nkv; ++j) {
-#endif
+        constexpr bool early = kEarly;  // Q and K 0.. already requested in the prologue
+        if (!early) {
+          const int row_q = bh * a.Np + qt * 128;
+          mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
+          tma_load_2d(sQ, &tm_q, q_full, 0, row_q);
+          bulk_load(sQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
+        }
+        for (int j = early ? SAGE3_EARLY_K : 0; j < nkv; ++j) {
           const int st = j % kKStages;
           const int row_k = bh * a.Np + j * 128;
           mbar_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
@@ -686,14 +688,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------- host
-template <int D, bool kSQ, bool kMX, bool kDirect>
-cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly>
+cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
   using L = Layout<D, kMX>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
@@ -706,8 +708,16 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_fwd_kernel<D, kSQ, kMX, kDirect><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
+  attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
   return cudaGetLastError();
+}
+
+template <int D, bool kSQ, bool kMX, bool kDirect>
+cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
+  if constexpr (!kSQ && !kDirect) {  // the north_star path: long sequences take the early-TMA instantiation
+    if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true>(a, stream);
+  }
+  return launch_dk<D, kSQ, kMX, kDirect, false>(a, stream);
 }
 
 }  // namespace
