@@ -49,6 +49,11 @@ constexpr float kMagicFB = 12582912.0f;
 constexpr float kOne127B = 0x1.020408p-7f;  // fl32(1/127)
 constexpr int kDQBufs = 3;  // dQ staging buffers per WG3 warp
 constexpr uint32_t kColS0 = 0, kColY = 128, kColS1 = 256, kColW = 384;
+// Regions Y and W alternate roles by tile parity: tile t holds dP(t) / dS(t) and then its dK partial in
+// R1(t), its dV partial in R2(t) = R1(t+1).  dP(t+1) then only waits for WG2 to read dV(t) (early), not for
+// WG3 to read dK(t) (late).
+__device__ __forceinline__ uint32_t r1col(int t) { return (t & 1) ? kColW : kColY; }
+__device__ __forceinline__ uint32_t r2col(int t) { return (t & 1) ? kColY : kColW; }
 
 // kind::i8: D s32, A/B signed; a_mn / b_mn select MN-major operands (bits 15 / 16).
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
@@ -227,7 +232,7 @@ struct BLayout {
   static constexpr int oRed = oX + 4 * 1024;       // 2 x 4 floats (tile amax reductions)
   static constexpr int oScl = oRed + 64;           // s_Q[Np/128], s_dO[Np/128] of the head (<= 1024 each)
   static constexpr int oBar = oScl + 2 * 4096;
-  static constexpr int kNumBars = 1 + 2 + 2 + 2 + 2 + 2 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 2 + 4;
+  static constexpr int kNumBars = 1 + 2 + 2 + 2 + 2 + 2 + 1 + 1 + 1 + 1 + 1 + 1 + 2 + 1 + 2 + 2 + 4;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kSmemAlloc = oTmem + 16 + 1024;
 };
@@ -254,10 +259,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
   uint64_t* ds_full = sp_empty + 1;   // WG1 -> MMA: dŜ in smem, S/P and dP/dS columns read
   uint64_t* sds_empty = ds_full + 1;  // MMA -> WG1: dK / dQ MMAs done reading dŜ
   uint64_t* dvp_full = sds_empty + 1;
-  uint64_t* dvp_empty = dvp_full + 1;
-  uint64_t* kq_full = dvp_empty + 1;
-  uint64_t* y_empty = kq_full + 1;    // WG3 -> MMA: dK partial read (dP of the next tile may overwrite it)
-  uint64_t* sb_empty = y_empty + 1;   // [2] WG3 -> MMA: dQ partial read from S buffer t % 2
+  uint64_t* dvp_empty = dvp_full + 1;  // [2] WG2 -> MMA: dV partial of tile t read from R2(t)
+  uint64_t* kq_full = dvp_empty + 2;
+  uint64_t* y_empty = kq_full + 1;    // [2] WG3 -> MMA: dK partial of tile t read from R1(t)
+  uint64_t* sb_empty = y_empty + 2;   // [2] WG3 -> MMA: dQ partial read from S buffer t % 2
   uint64_t* x_full = sb_empty + 2;    // [4] WG1 -> WG2 / WG3: s_P, s_dS, rowsum(dS) of tile t in slot t % 4
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
   float* s_km = reinterpret_cast<float*>(smem + L::oKm);
@@ -289,9 +294,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
     mbar_init(ds_full, 4);
     mbar_init(sds_empty, 1);
     mbar_init(dvp_full, 1);
-    mbar_init(dvp_empty, 4);
+    mbar_init(&dvp_empty[0], 4);
+    mbar_init(&dvp_empty[1], 4);
     mbar_init(kq_full, 1);
-    mbar_init(y_empty, 4);
+    mbar_init(&y_empty[0], 4);
+    mbar_init(&y_empty[1], 4);
     for (int s = 0; s < 4; ++s) mbar_init(&x_full[s], 128);
     fence_mbar_init();
   }
@@ -377,27 +384,27 @@ __global__ void __launch_bounds__(kBThreads, 1)
                     make_smem_desc(sK + 32 * ks, 16, kI8Sbo, kI8Layout), id_s, ks > 0);
           mma_commit(&s_full[st]);
         };
-        auto issue_dp = [&](int t) {
+        auto issue_dp = [&](int t) {  // into R1(t) = R2(t-1): after WG2 has read the dV partial of t-1
           mbar_wait(&do_full[0], (uint32_t)t & 1u);
-          mbar_wait(y_empty, ((uint32_t)t & 1u) ^ 1u);
+          if (t > 0) mbar_wait(&dvp_empty[(t - 1) & 1], (uint32_t)((t - 1) >> 1) & 1u);
           tc_fence_after();
 #pragma unroll 1
           for (int ks = 0; ks < D / 16; ++ks) {
             const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-            mma_f16b(tbase + kColY, make_smem_desc(sDO + off, 16, 1024, kLayoutSw128),
+            mma_f16b(tbase + r1col(t), make_smem_desc(sDO + off, 16, 1024, kLayoutSw128),
                      make_smem_desc(sV + off, 16, 1024, kLayoutSw128), id_dp_rt, ks > 0);
           }
           mma_commit(&do_full[1]);
           mma_commit(dp_full);
         };
-        auto issue_dv = [&](int t) {
+        auto issue_dv = [&](int t) {  // into R2(t) = R1(t-1): after WG3 has read the dK partial of t-1
           mbar_wait(p_full, (uint32_t)t & 1u);
-          mbar_wait(dvp_empty, ((uint32_t)t & 1u) ^ 1u);
+          if (t > 0) mbar_wait(&y_empty[(t - 1) & 1], (uint32_t)((t - 1) >> 1) & 1u);
           mbar_wait(&dq8_full[0], (uint32_t)t & 1u);
           tc_fence_after();
 #pragma unroll 1
           for (int ks = 0; ks < 4; ++ks)
-            mma_i8b(tbase + kColW, make_smem_desc(sP + 4096 * ks, 8192, 1024, kLayoutSw128),
+            mma_i8b(tbase + r2col(t), make_smem_desc(sP + 4096 * ks, 8192, 1024, kLayoutSw128),
                     make_smem_desc(sDOq + kI8KStep * ks, 8192, kI8Sbo, kI8Layout), id_dvk, ks > 0);
           mma_commit(&dq8_full[1]);
           mma_commit(sp_empty);
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
           tc_fence_after();
 #pragma unroll 1
           for (int ks = 0; ks < 4; ++ks)  // dK partial: A = dŜᵀ (keys x queries, MN-major), B = Q̂_i (MN-major)
-            mma_i8b(tbase + kColY, make_smem_desc(sDS + 4096 * ks, 8192, 1024, kLayoutSw128),
+            mma_i8b(tbase + r1col(t), make_smem_desc(sDS + 4096 * ks, 8192, 1024, kLayoutSw128),
                     make_smem_desc(sQ + kI8KStep * ks, 8192, kI8Sbo, kI8Layout), id_dvk, ks > 0);
 #pragma unroll 1
           for (int ks = 0; ks < 4; ++ks)  // dQ partial: A = dŜ (queries x keys, K-major), B = K̂_j (MN-major)
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       constexpr bool masked = decltype(masked_tag)::value;
       const int i = i0 + t, st = t & 1;
       const int q_row = i * 128 + r;
-      const uint32_t tS = lane_base + (st ? kColS1 : kColS0), tY = lane_base + kColY;
+      const uint32_t tS = lane_base + (st ? kColS1 : kColS0), tY = lane_base + r1col(t);
       SAGE3_TRACE_EV(1, t, 0);
       mbar_wait(&q_full[st], (uint32_t)(t >> 1) & 1u);
       const uint32_t ld = smem_u32(smem + L::oLD + st * 1024) + 4 * r;
@@ -628,7 +635,6 @@ __global__ void __launch_bounds__(kBThreads, 1)
     setmaxnreg_inc<kBRegDV>();
     const int r = threadIdx.x - 256;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-    const uint32_t tW = lane_base + kColW;
     uint8_t* stage = smem + L::oDQ + (warp & 3) * (kDQBufs * 2048);
     int nflush = 0;
     f2 acc[D / 2];
@@ -648,13 +654,13 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #pragma unroll
       for (int cc = 0; cc < D / 16; ++cc) {
         uint32_t v[16];
-        tmem_ld16(tW + 16 * cc, v);
+        tmem_ld16(lane_base + r2col(t) + 16 * cc, v);
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[8 * cc + e] = ffma2(i2f2b(v[2 * e], v[2 * e + 1]), w2, acc[8 * cc + e]);
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(dvp_empty);
+      if (lane == 0) mbar_arrive(&dvp_empty[t & 1]);
       SAGE3_TRACE_EV(5, t, 2);
       const float wq = __fmul_rn(s_ds, sk_j);
       mbar_wait(kq_full, (uint32_t)t & 1u);
@@ -696,8 +702,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #pragma unroll
         for (int cc = 0; cc < D / 16; cc += 2) {
           uint32_t va[16], vb[16];
-          tmem_ld_32x32b_x16(lane_base + kColY + 16 * cc, va);
-          tmem_ld_32x32b_x16(lane_base + kColY + 16 * cc + 16, vb);
+          tmem_ld_32x32b_x16(lane_base + r1col(t) + 16 * cc, va);
+          tmem_ld_32x32b_x16(lane_base + r1col(t) + 16 * cc + 16, vb);
           tmem_ld_wait_regs(va);
           tmem_ld_wait_regs(vb);
 #pragma unroll
@@ -709,7 +715,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(y_empty);
+      if (lane == 0) mbar_arrive(&y_empty[t & 1]);
       SAGE3_TRACE_EV(4, t, 2);
       // dQ partial of (i, j): MM(dŜ, K̂_j)·s_dS·s_K + rowsum(dS)·K_m (Alg3 L10), columns [D/2, D)
       flush_dq<D / 32>(&tm_dqacc, lane_base + (st ? kColS1 : kColS0), D / 2, stage, nflush, s_km,
