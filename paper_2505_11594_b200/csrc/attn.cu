@@ -69,8 +69,17 @@ constexpr int kThreads = 512;
 #define SAGE3_REG_SOFTMAX 144
 #define SAGE3_REG_CORRECTION 192
 #endif
+#ifndef SAGE3_REG_SOFTMAX_D64  // d = 64: O is 64 floats, so the correction warpgroup needs fewer registers
+#define SAGE3_REG_SOFTMAX_D64 176   // (same-box A/B on C3: 176/128 726 TOPS, 168/144 717, 144/192 722)
+#define SAGE3_REG_CORRECTION_D64 128
+#endif
 constexpr uint32_t kRegWG0 = SAGE3_REG_WG0, kRegSoftmax = SAGE3_REG_SOFTMAX, kRegCorrection = SAGE3_REG_CORRECTION;
 static_assert(kRegWG0 + 2 * kRegSoftmax + kRegCorrection <= 512, "register budget");
+static_assert(kRegWG0 + 2 * SAGE3_REG_SOFTMAX_D64 + SAGE3_REG_CORRECTION_D64 <= 512, "register budget (d = 64)");
+template <int D>
+constexpr uint32_t reg_softmax() { return D == 64 ? SAGE3_REG_SOFTMAX_D64 : kRegSoftmax; }
+template <int D>
+constexpr uint32_t reg_correction() { return D == 64 ? SAGE3_REG_CORRECTION_D64 : kRegCorrection; }
 
 // TMEM column map (512 columns allocated): three 128-column buffers; tile j uses buffer j % 3 first for
 // S_j (MMA), then — once the softmax has read S_j — for PV_j (MMA), which the correction warpgroup reads
@@ -340,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (wg >= 2) {
     // -------------------------------------------------------------------- softmax + two-level P quant
-    setmaxnreg_inc<kRegSoftmax>();
+    setmaxnreg_inc<reg_softmax<D>()>();
     const int par = wg - 2;                 // this warpgroup's KV-tile parity
     const int r = threadIdx.x - 128 * wg;   // query row in the tile == TMEM lane
     const int q_row = qt * 128 + r;
@@ -613,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // exceeds it by more than 2^8 in weight), so tile j enters with weight
     //   w_j = 2^{sl2 (tmax_j − mref)} / 2688  (= s_P1 · Π α relative to mref)
     // which is Alg1 L9-L11 up to fp32 rounding: O/l and lse are independent of the reference.
-    setmaxnreg_inc<kRegCorrection>();
+    setmaxnreg_inc<reg_correction<D>()>();
     const int r = threadIdx.x - 128;
     const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
