@@ -19,9 +19,11 @@
 //   final   dQ = scale·dQ_acc (the softmax scale multiplies S inside the softmax, reading b7).
 //
 // Warp roles of the main kernel (16 warps): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
-// WG1 element-wise work (P, ψ(P), dS, ψ(dS), rowsum), WG2 dV accumulation + store, WG3 dK accumulation,
+// WG1 element-wise work (P, ψ(P), dS, ψ(dS), rowsum), WG2 dV accumulation + store, WG3 dK accumulation +
 // dQ flush + dK store.  TMEM (512 columns): S buffers at 0 and 256 (tile t uses t % 2; its dQ partial is
-// written over it), dP / dK partial at 128, dV partial at 384.
+// written over it); regions Y (128) and W (384) alternate by tile parity between "dP / dS, then the dK partial"
+// (R1) and "the dV partial" (R2), so the next tile's dP never waits for the dK read.
+// WG2 and WG3 each flush half of every dQ partial.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
