@@ -43,6 +43,9 @@ namespace {
 
 using namespace ptx;
 
+#ifndef SAGE3_BWD_I2F
+#define SAGE3_BWD_I2F 1  // int32 -> fp32 by cvt (I2F) instead of the magic-number add
+#endif
 constexpr int kBThreads = 512;
 constexpr uint32_t kBRegWG0 = 40, kBRegElem = 136, kBRegDV = 160, kBRegDK = 176;
 static_assert(kBRegWG0 + kBRegElem + kBRegDV + kBRegDK <= 512, "register budget");
@@ -86,9 +89,13 @@ __device__ __forceinline__ void mma_f16b(uint32_t d_tmem, uint64_t a_desc, uint6
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ f2 i2f2b(uint32_t a, uint32_t b) {  // exact int32 -> fp32 for |x| < 2^22
+__device__ __forceinline__ f2 i2f2b(uint32_t a, uint32_t b) {  // exact int32 -> fp32 (|x| < 2^24): I2F
+#if SAGE3_BWD_I2F
+  return make_float2(__int2float_rn((int)a), __int2float_rn((int)b));
+#else
   return fadd2(make_float2(__uint_as_float(a + kMagicIB), __uint_as_float(b + kMagicIB)),
                make_float2(-kMagicFB, -kMagicFB));
+#endif
 }
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
