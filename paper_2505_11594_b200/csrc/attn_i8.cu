@@ -29,6 +29,10 @@ using namespace ptx;
 #ifndef SAGE3_I8_ROLLED
 #define SAGE3_I8_ROLLED 1
 #endif
+#ifndef SAGE3_POLY_MASK_I8  // exp pairs on the FMA-pipe polynomial in the INT8 softmax; after the I2F change
+#define SAGE3_POLY_MASK_I8 0  // all-MUFU is best (A/B at N = 32K: none 1312 TOPS, 1/16 1278, 1/8 1297, 1/4 1268)
+#endif
+constexpr uint32_t kPolyMaskI8 = SAGE3_POLY_MASK_I8;
 #ifndef SAGE3_I8_I2F
 #define SAGE3_I8_I2F 1  // int32 -> fp32 by cvt (I2F) instead of the magic-number add
 #endif
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
             x.x = (32 * cc + 2 * i > lim) ? -INFINITY : x.x;
             x.y = (32 * cc + 2 * i + 1 > lim) ? -INFINITY : x.y;
           }
-          y[i] = ((kPolyMask >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          y[i] = ((kPolyMaskI8 >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
         }
         uint32_t w[8];
 #pragma unroll
