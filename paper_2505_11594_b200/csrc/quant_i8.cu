@@ -33,10 +33,15 @@ __device__ __forceinline__ int8_t enc(float x, float r) {
   return (int8_t)(int)v;
 }
 
+#ifndef SAGE3_I8Q_THREADS
+#define SAGE3_I8Q_THREADS 512  // (0.560 ms vs 0.574 ms with 256 at N = 32K, d = 128)
+#endif
+constexpr int kQT = SAGE3_I8Q_THREADS;  // threads per (block, head, tensor) CTA
+
 template <typename T, int D>
-__global__ void __launch_bounds__(256) i8_quant_kernel(const I8Args a) {
-  constexpr int kVec = D / 8, kIt = 128 * kVec / 256;  // 16-byte vectors per row; vectors per thread
-  __shared__ float s_red[8];
+__global__ void __launch_bounds__(kQT) i8_quant_kernel(const I8Args a) {
+  constexpr int kVec = D / 8, kIt = 128 * kVec / kQT;  // 16-byte vectors per row; vectors per thread
+  __shared__ float s_red[kQT / 32];
   __shared__ __align__(16) int8_t s_vt[D * 128];  // V̂ codes staging: [token][channel], swizzled
   const int chunk = blockIdx.x, bh = blockIdx.y, tensor = blockIdx.z;  // 0 Q, 1 K, 2 V
   const int b = bh / a.H, h = bh % a.H, t = threadIdx.x;
@@ -56,7 +61,7 @@ __global__ void __launch_bounds__(256) i8_quant_kernel(const I8Args a) {
   bool finite = true;
 #pragma unroll
   for (int it = 0; it < kIt; ++it) {
-    const int row = (it * 256 + t) / kVec, n = chunk * 128 + row;
+    const int row = (it * kQT + t) / kVec, n = chunk * 128 + row;
     if (n < a.N) {
       const uint4 u = *reinterpret_cast<const uint4*>(base + (int64_t)n * sn + cv * 8);
       const T* hv = reinterpret_cast<const T*>(&u);
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(256) i8_quant_kernel(const I8Args a) {
   __syncthreads();
   amax = s_red[0];
 #pragma unroll
-  for (int w = 1; w < 8; ++w) amax = fmaxf(amax, s_red[w]);
+  for (int w = 1; w < kQT / 32; ++w) amax = fmaxf(amax, s_red[w]);
   const float s = __fmul_rn(amax, kOne127);
   const float r = s != 0.0f ? __frcp_rn(s) : 0.0f;
   const int nch = a.Np >> 7;
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(256) i8_quant_kernel(const I8Args a) {
     int8_t* dst = (tensor == 0 ? a.q8 : a.k8) + ((int64_t)bh * a.Np + chunk * 128) * D;
 #pragma unroll
     for (int it = 0; it < kIt; ++it) {
-      const int row = (it * 256 + t) / kVec;
+      const int row = (it * kQT + t) / kVec;
       uint32_t w[2];
       int8_t* bytes = reinterpret_cast<int8_t*>(w);
 #pragma unroll
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(256) i8_quant_kernel(const I8Args a) {
     // transposed smem stores were 16-way bank conflicted (ncu: 7.9M conflicts per launch at N = 4K).
 #pragma unroll
     for (int it = 0; it < kIt; ++it) {
-      const int row = (it * 256 + t) / kVec;
+      const int row = (it * kQT + t) / kVec;
       uint32_t w[2];
       int8_t* bytes = reinterpret_cast<int8_t*>(w);
 #pragma unroll
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(256) i8_quant_kernel(const I8Args a) {
       *reinterpret_cast<uint2*>(s_vt + row * D + ((cv ^ ((row >> 4) & 7)) * 8)) = make_uint2(w[0], w[1]);
     }
     __syncthreads();
-    for (int i = t; i < (D / 4) * 8; i += 256) {
+    for (int i = t; i < (D / 4) * 8; i += kQT) {
       const int q = i & 7, c4 = i >> 3;  // 16-token group, channel quad
       uint32_t w[16];
 #pragma unroll
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(256) i8_quant_kernel(const I8Args a) {
 template <typename T, int D>
 cudaError_t launch_i8_t(const I8Args& a, cudaStream_t stream) {
   dim3 grid(a.Np / 128, a.B * a.H, 3);
-  i8_quant_kernel<T, D><<<grid, 256, 0, stream>>>(a);
+  i8_quant_kernel<T, D><<<grid, kQT, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
