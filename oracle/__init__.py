@@ -73,6 +73,9 @@ def lib():
             L.oracle_attn_fwd_fmt.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p,
                                               fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                               ctypes.c_int, ip, ctypes.c_int, dp, dp]
+            L.oracle_attn_fwd_amb.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p,
+                                              fp, fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                              ctypes.c_int, ip, ctypes.c_int, dp, dp, ctypes.c_double, dp]
             L.oracle_dequant_fmt.argtypes = [u8p, u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
             L.oracle_qmean_tile.argtypes = [fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, fp]
             L.oracle_attn_fwd_sq.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, u8p, u8p, u8p, u8p, u8p,
@@ -97,6 +100,8 @@ def lib():
             L.sb_quantize_head.argtypes = [fp, fp, fp, ctypes.c_int, ctypes.c_int, i8p, i8p, i8p, fp, fp, fp, fp]
             L.sb_attn_fwd.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i8p, i8p, i8p, fp, fp, fp,
                                       ctypes.c_int, ctypes.c_double, ip, ctypes.c_int, dp, dp]
+            L.sb_attn_fwd_amb.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i8p, i8p, i8p, fp, fp, fp,
+                                      ctypes.c_int, ctypes.c_double, ip, ctypes.c_int, dp, dp, ctypes.c_double, dp]
             L.sb_bwd_head.argtypes = [ctypes.c_int, ctypes.c_int, i8p, i8p, fp, fp, fp, fp, fp, fp, fp,
                                       ctypes.c_int, ctypes.c_double, dp, dp, dp]
             L.oracle_e4m3_encode_array.argtypes = [fp, ctypes.c_int64, u8p]
@@ -282,9 +287,11 @@ def qmean_tile(Q, tile: int) -> np.ndarray:
 
 
 def attn_fwd(heads: list[QuantizedHead], *, causal: bool, scale: float, rows=None, bkv: int = 128,
-             p_mode: int = PMODE_TWO_LEVEL, want_lse: bool = False):
+             p_mode: int = PMODE_TWO_LEVEL, want_lse: bool = False, amb_delta: float | None = None):
     """Alg1 L6-L13 on quantized heads (all same N, d; smoothing Q iff the heads carry q_mean/ks).
-    Returns O [BH][nrows][d] fp64 (and lse)."""
+    Returns O [BH][nrows][d] fp64 (and lse).  With amb_delta: also amb [BH][nrows][d], the bound on how far O
+    can move when every P quantization decision is re-taken on values within a relative amb_delta (test
+    infrastructure for the GPU parity bound; see oracle_attn_fwd_amb).  Returns (O, lse, amb) then."""
     N, d, Np = heads[0].N, heads[0].d, heads[0].Np
     BH = len(heads)
     rows = np.arange(N, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
@@ -294,12 +301,16 @@ def attn_fwd(heads: list[QuantizedHead], *, causal: bool, scale: float, rows=Non
     qm, kf = (cat("q_mean"), cat("ks")) if sq else (None, None)
     O = np.zeros((BH, rows.shape[0], d), np.float64)
     lse = np.zeros((BH, rows.shape[0]), np.float64)
+    amb = np.zeros((BH, rows.shape[0], d), np.float64) if amb_delta is not None else None
     u8, fp = ctypes.c_uint8, ctypes.c_float
-    lib().oracle_attn_fwd_fmt(BH, N, d, _p(qc, u8), _p(qs, u8), _p(kc, u8), _p(ks, u8), _p(vc, u8), _p(vs, u8),
-                             _p(qm, fp) if sq else None, _p(kf, fp) if sq else None, heads[0].fmt, bkv,
-                             1 if causal else 0,
-                             float(scale), p_mode, _p(rows, ctypes.c_int), rows.shape[0], _p(O, ctypes.c_double),
-                             _p(lse, ctypes.c_double))
+    lib().oracle_attn_fwd_amb(BH, N, d, _p(qc, u8), _p(qs, u8), _p(kc, u8), _p(ks, u8), _p(vc, u8), _p(vs, u8),
+                              _p(qm, fp) if sq else None, _p(kf, fp) if sq else None, heads[0].fmt, bkv,
+                              1 if causal else 0,
+                              float(scale), p_mode, _p(rows, ctypes.c_int), rows.shape[0], _p(O, ctypes.c_double),
+                              _p(lse, ctypes.c_double), float(amb_delta or 0.0),
+                              _p(amb, ctypes.c_double) if amb is not None else None)
+    if amb is not None:
+        return O, lse, amb
     return (O, lse) if want_lse else O
 
 
@@ -382,18 +393,24 @@ def sb_quantize_head(Q, K, V) -> SbHead:
     return h
 
 
-def sb_attn_fwd(heads: list[SbHead], *, causal: bool, scale: float, rows=None, want_lse: bool = False):
-    """Alg2 L6-L14 on quantized heads: O [BH][nrows][d] fp64 (and lse = scale·m + ln l)."""
+def sb_attn_fwd(heads: list[SbHead], *, causal: bool, scale: float, rows=None, want_lse: bool = False,
+                amb_delta: float | None = None):
+    """Alg2 L6-L14 on quantized heads: O [BH][nrows][d] fp64 (and lse = scale·m + ln l).  With amb_delta also the
+    decision-sensitivity bound amb [BH][nrows][d] (test infrastructure, see sb_attn_fwd_amb): returns (O, lse, amb)."""
     N, d, Np = heads[0].N, heads[0].d, heads[0].Np
     rows = np.arange(N, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
     cat = lambda name: np.ascontiguousarray(np.concatenate([getattr(h, name) for h in heads]))  # noqa: E731
     q, k, v, sq, sk, sv = (cat(n) for n in ("q", "k", "v", "sq", "sk", "sv"))
     O = np.zeros((len(heads), len(rows), d), np.float64)
     lse = np.zeros((len(heads), len(rows)), np.float64)
-    lib().sb_attn_fwd(len(heads), N, d, _p(q, ctypes.c_int8), _p(k, ctypes.c_int8), _p(v, ctypes.c_int8),
-                      _p(sq, ctypes.c_float), _p(sk, ctypes.c_float), _p(sv, ctypes.c_float), int(causal),
-                      float(scale), _p(rows, ctypes.c_int), len(rows), _p(O, ctypes.c_double),
-                      _p(lse, ctypes.c_double))
+    amb = np.zeros_like(O) if amb_delta is not None else None
+    lib().sb_attn_fwd_amb(len(heads), N, d, _p(q, ctypes.c_int8), _p(k, ctypes.c_int8), _p(v, ctypes.c_int8),
+                          _p(sq, ctypes.c_float), _p(sk, ctypes.c_float), _p(sv, ctypes.c_float), int(causal),
+                          float(scale), _p(rows, ctypes.c_int), len(rows), _p(O, ctypes.c_double),
+                          _p(lse, ctypes.c_double), float(amb_delta or 0.0),
+                          _p(amb, ctypes.c_double) if amb is not None else None)
+    if amb is not None:
+        return O, lse, amb
     return (O, lse) if want_lse else O
 
 

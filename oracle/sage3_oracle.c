@@ -360,6 +360,49 @@ EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* co
 }
 
 /* ------------------------------------------------------------------------------------------------
+ * Decision sensitivity of φ (TEST INFRASTRUCTURE for the GPU parity bound; it does not
+ * change any result above).  The GPU evaluates P̃2 (or P̃) with its own exp2 and fp32 S accumulation, so
+ * its values differ from the oracle's by a relative amount below `delta`.  When a value sits that close
+ * to an E2M1 rounding midpoint (or a block amax/6 that close to an E4M3 midpoint / power of two), the two
+ * sides may legitimately pick adjacent codes.  For every element this returns dq[i] = the spread of its
+ * dequantized value q_i·s over all inputs within a relative delta of x (every element and the block amax
+ * moving independently); dq[i] = 0 whenever the decision is the same for all of them.  Both codecs and
+ * the scale rule are monotone, so the extreme perturbations bound every reachable decision.
+ * ------------------------------------------------------------------------------------------------ */
+static double phi_scale_of(double amax, int fmt) {
+  const float s32 = (float)amax * (1.0f / 6.0f);
+  if (!fmt) return oracle_e4m3_decode(oracle_e4m3_encode(s32));
+  if (s32 == 0.0f) return 0.0;
+  int e;
+  double fr = frexp((double)s32, &e);
+  int p = (fr == 0.5) ? e - 1 : e;
+  if (p < -127) p = -127;
+  if (p > 127) p = 127;
+  return ldexp(1.0, p);
+}
+EXPORT void oracle_phi_sensitivity(const float* x, int G, int fmt, double delta, double* dq) {
+  double amax = 0.0;
+  for (int i = 0; i < G; ++i)
+    if (fabs((double)x[i]) > amax) amax = fabs((double)x[i]);
+  const double sc[2] = {phi_scale_of(amax * (1.0 - delta), fmt), phi_scale_of(amax * (1.0 + delta), fmt)};
+  for (int i = 0; i < G; ++i) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        double v = 0.0;
+        if (sc[a] != 0.0) {
+          const float xv = (float)((double)x[i] * (b ? 1.0 + delta : 1.0 - delta));
+          const float y = fmt ? (float)((double)xv / sc[a]) : xv * (1.0f / (float)sc[a]);
+          v = oracle_e2m1_decode(oracle_e2m1_encode(y)) * sc[a];
+        }
+        if (v < lo) lo = v;
+        if (v > hi) hi = v;
+      }
+    dq[i] = hi - lo;
+  }
+}
+
+/* ------------------------------------------------------------------------------------------------
  * NEXT #2 variant (reading n1; NOT the paper's Alg1 L10): two-level P whose first level is a
  * lazily moved per-row reference r instead of each tile's own row max.  Per KV tile j, after S (Alg1 L8):
  *   if r = -inf or log2(e)·scale·(tmax_j - r) > LAZY_TAU:  O *= exp(scale(r - tmax_j)), l *= the same,
@@ -376,14 +419,17 @@ EXPORT float oracle_two_level_row(const float* P, int n, int p_mode, uint8_t* co
 #define LAZY_TOP 10.5 /* 2688 * 2^-8, exact */
 static void attn_row_lazy(const double* Qrow, const double* Kd, const double* Vt, int N, int Np, int d, int Bkv,
                           int causal, int qi, double scale, const float* qbar, const float* Ks, int fmt, double* O,
-                          double* lse) {
+                          double* lse, double delta, double* amb) {
   const int G = fmt ? 32 : 16;
   double r = -INFINITY, l = 0.0;
   double* S = (double*)malloc(sizeof(double) * (size_t)Bkv);
   float* P2 = (float*)malloc(sizeof(float) * (size_t)Bkv);
   uint8_t* pc = (uint8_t*)malloc((size_t)Bkv);
   uint8_t* ps = (uint8_t*)malloc((size_t)Bkv / 16 + 1);
+  double* dq = amb ? (double*)malloc(sizeof(double) * (size_t)Bkv) : NULL;
   for (int c = 0; c < d; ++c) O[c] = 0.0;
+  if (amb)
+    for (int c = 0; c < d; ++c) amb[c] = 0.0;
   int kv_end = causal ? (qi + 1 < N ? qi + 1 : N) : N;
   for (int j0 = 0; j0 < kv_end; j0 += Bkv) {
     double tmax = -INFINITY;
@@ -406,6 +452,8 @@ static void attn_row_lazy(const double* Qrow, const double* Kd, const double* Vt
     if (r == -INFINITY || (tmax - r) * scale / log(2.0) > LAZY_TAU) { /* move the reference */
       double a = (r == -INFINITY) ? 0.0 : exp(scale * (r - tmax));
       for (int c = 0; c < d; ++c) O[c] *= a;
+      if (amb)
+        for (int c = 0; c < d; ++c) amb[c] *= a;
       l *= a;
       r = tmax;
     }
@@ -416,7 +464,11 @@ static void attn_row_lazy(const double* Qrow, const double* Kd, const double* Vt
     for (int b = 0; b < Bkv; b += G) {
       if (fmt) oracle_phi_mxfp4(&P2[b], &pc[b], &ps[b / G]);
       else oracle_phi_nvfp4(&P2[b], &pc[b], &ps[b / G]);
+      if (amb) oracle_phi_sensitivity(&P2[b], G, fmt, delta, &dq[b]);
     }
+    if (amb)
+      for (int c = 0; c < d; ++c)
+        for (int t = 0; t < Bkv && j0 + t < Np; ++t) amb[c] += dq[t] * fabs(Vt[(size_t)c * Np + j0 + t]);
     for (int c = 0; c < d; ++c) {
       double pv = 0.0;
       for (int t = 0; t < Bkv; ++t) {
@@ -429,7 +481,10 @@ static void attn_row_lazy(const double* Qrow, const double* Kd, const double* Vt
     }
   }
   for (int c = 0; c < d; ++c) O[c] /= l;
+  if (amb)
+    for (int c = 0; c < d; ++c) amb[c] /= l;
   if (lse) *lse = scale * r + log(l / LAZY_TOP);
+  free(dq);
   free(S);
   free(P2);
   free(pc);
@@ -449,18 +504,23 @@ static void attn_row_lazy(const double* Qrow, const double* Kd, const double* Vt
  * ------------------------------------------------------------------------------------------------ */
 static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int N, int Np, int d, int Bkv,
                      int causal, int qi, double scale, int p_mode, const float* qbar, const float* Ks, int fmt,
-                     double* O, double* lse) {
+                     double* O, double* lse, double delta, double* amb) {
   if (p_mode == PMODE_LAZY) {
-    attn_row_lazy(Qrow, Kd, Vt, N, Np, d, Bkv, causal, qi, scale, qbar, Ks, fmt, O, lse);
+    attn_row_lazy(Qrow, Kd, Vt, N, Np, d, Bkv, causal, qi, scale, qbar, Ks, fmt, O, lse, delta, amb);
     return;
   }
+  const int G = fmt ? 32 : 16;
   double m = -INFINITY, l = 0.0;
   double* S = (double*)malloc(sizeof(double) * (size_t)Bkv);
   float* Pt = (float*)malloc(sizeof(float) * (size_t)Bkv);
   double* Pq = (double*)malloc(sizeof(double) * (size_t)Bkv);
   uint8_t* pc = (uint8_t*)malloc((size_t)Bkv);
   uint8_t* ps = (uint8_t*)malloc((size_t)Bkv / 16 + 1);
+  double* dq = amb ? (double*)malloc(sizeof(double) * (size_t)Bkv) : NULL;
+  float p2[32];
   for (int c = 0; c < d; ++c) O[c] = 0.0;
+  if (amb)
+    for (int c = 0; c < d; ++c) amb[c] = 0.0;
   int kv_end = causal ? (qi + 1 < N ? qi + 1 : N) : N;
   for (int j0 = 0; j0 < kv_end; j0 += Bkv) {
     /* Alg1 L8: S_ij = FP4MM(Q̂_i, s_Q, K̂_j, s_K) — exact in fp64 */
@@ -500,6 +560,11 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
       sP1 = (double)oracle_two_level_row_fmt(Pt, Bkv, p_mode, fmt, pc, ps);
       for (int t = 0; t < Bkv; ++t)
         Pq[t] = oracle_e2m1_decode(pc[t]) * (fmt ? ldexp(1.0, (int)ps[t / 32] - 127) : oracle_e4m3_decode(ps[t / 16]));
+      if (amb && sP1 != 0.0) /* the decisions' sensitivity on the values φ saw: P̃2 = fl32(P̃/s_P1), or P̃ (direct) */
+        for (int b = 0; b < Bkv; b += G) {
+          for (int i = 0; i < G; ++i) p2[i] = p_mode == PMODE_DIRECT ? Pt[b + i] : Pt[b + i] / (float)sP1;
+          oracle_phi_sensitivity(p2, G, fmt, delta, &dq[b]);
+        }
     }
     /* Alg1 L11: O = diag(alpha) O + FP4MM(P̂2, s_P2, V̂, s_V) * s_P1 (inner sum exact in fp64) */
     for (int c = 0; c < d; ++c) {
@@ -511,11 +576,22 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
       }
       O[c] = alpha * O[c] + pv * sP1;
     }
+    if (amb) {
+      for (int c = 0; c < d; ++c) {
+        double a = 0.0;
+        if (p_mode != PMODE_NONE && sP1 != 0.0)
+          for (int t = 0; t < Bkv && j0 + t < Np; ++t) a += dq[t] * fabs(Vt[(size_t)c * Np + j0 + t]);
+        amb[c] = alpha * amb[c] + a * sP1;
+      }
+    }
     m = m_new;
   }
   /* Alg1 L13: O_i = diag(l)^-1 O */
   for (int c = 0; c < d; ++c) O[c] /= l;
+  if (amb)
+    for (int c = 0; c < d; ++c) amb[c] /= l;
   if (lse) *lse = scale * m + log(l);
+  free(dq);
   free(S);
   free(Pt);
   free(Pq);
@@ -527,10 +603,11 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
  * oracle_quantize_head, stacked per head).  rows[nrows] selects the query rows evaluated (rows are
  * independent, so a row sample is exact for those rows).  O: [BH][nrows][d], lse: [BH][nrows] (nullable).
  * OpenMP over (head, row). */
-EXPORT void oracle_attn_fwd_fmt(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
+EXPORT void oracle_attn_fwd_amb(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
                                 const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
                                 const uint8_t* v_sf, const float* q_mean, const float* ks, int fmt, int Bkv, int causal,
-                                double scale, int p_mode, const int* rows, int nrows, double* O, double* lse) {
+                                double scale, int p_mode, const int* rows, int nrows, double* O, double* lse,
+                                double delta, double* amb) {
   const int Np = (N + 127) / 128 * 128;
   const int G = fmt ? 32 : 16;
   const int C = d / G;
@@ -548,12 +625,21 @@ EXPORT void oracle_attn_fwd_fmt(int BH, int N, int d, const uint8_t* q_codes, co
       int qi = rows[r];
       attn_row(&Qd[(size_t)qi * d], Kd, Vt, N, Np, d, Bkv, causal, qi, scale, p_mode,
                qm_h ? qm_h + (size_t)(qi / 128) * d : NULL, ks_h, fmt, &O[((size_t)h * nrows + r) * d],
-               lse ? &lse[(size_t)h * nrows + r] : NULL);
+               lse ? &lse[(size_t)h * nrows + r] : NULL, delta, amb ? &amb[((size_t)h * nrows + r) * d] : NULL);
     }
     free(Qd);
     free(Kd);
     free(Vt);
   }
+}
+
+/* The same without the decision-sensitivity output. */
+EXPORT void oracle_attn_fwd_fmt(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
+                                const uint8_t* k_codes, const uint8_t* k_sf, const uint8_t* v_codes,
+                                const uint8_t* v_sf, const float* q_mean, const float* ks, int fmt, int Bkv, int causal,
+                                double scale, int p_mode, const int* rows, int nrows, double* O, double* lse) {
+  oracle_attn_fwd_amb(BH, N, d, q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, q_mean, ks, fmt, Bkv, causal, scale,
+                      p_mode, rows, nrows, O, lse, 0.0, NULL);
 }
 
 EXPORT void oracle_attn_fwd_sq(int BH, int N, int d, const uint8_t* q_codes, const uint8_t* q_sf,
@@ -590,7 +676,7 @@ EXPORT void oracle_attn_fwd_float(int N, int d, const float* Q, const float* K, 
     double* Qrow = (double*)malloc(sizeof(double) * (size_t)d);
     for (int c = 0; c < d; ++c) Qrow[c] = Q[(size_t)rows[r] * d + c];
     attn_row(Qrow, Kd, Vt, N, Np, d, Bkv, causal, rows[r], scale, p_mode, NULL, NULL, 0, &O[(size_t)r * d],
-             lse ? &lse[r] : NULL);
+             lse ? &lse[r] : NULL, 0.0, NULL);
     free(Qrow);
   }
   free(Kd);

@@ -88,11 +88,13 @@ EXPORT void sb_quantize_head(const float* Q, const float* K, const float* V, int
  * exp(rowmax(S) - m)/127 computed from P̃, reusing the max), P̂ = RNE(fl32(P̃ / s_P)) in [0, 127]. */
 static void sb_fwd_row(const int8_t* q, const int8_t* k, const int8_t* v, const float* sq, const float* sk,
                        const float* sv, int N, int Np, int d, int causal, int qi, double scale, double* O,
-                       double* lse) {
+                       double* lse, double delta, double* amb) {
   double m = -INFINITY, l = 0.0;
-  double S[SB_BLK], Pq[SB_BLK];
+  double S[SB_BLK], Pq[SB_BLK], dq[SB_BLK];
   float Pt[SB_BLK];
   for (int c = 0; c < d; ++c) O[c] = 0.0;
+  if (amb)
+    for (int c = 0; c < d; ++c) amb[c] = 0.0;
   const int kv_end = causal ? (qi + 1 < N ? qi + 1 : N) : N;
   for (int j0 = 0; j0 < kv_end; j0 += SB_BLK) {
     double tmax = -INFINITY;
@@ -119,6 +121,14 @@ static void sb_fwd_row(const int8_t* q, const int8_t* k, const int8_t* v, const 
     l = alpha * l + rowsum;
     const float sP = pmax / 127.0f; /* Alg2 L10, per token */
     for (int t = 0; t < SB_BLK; ++t) Pq[t] = (sP > 0.0f) ? (double)nearbyintf(Pt[t] / sP) : 0.0;
+    /* Decision sensitivity (TEST INFRASTRUCTURE for the GPU element-wise parity bound, as
+     * oracle_phi_sensitivity in sage3_oracle.c): the spread of the INT8 code of P̃/s_P over inputs within a
+     * relative delta; 0 unless the value sits that close to a rounding midpoint. */
+    if (amb)
+      for (int t = 0; t < SB_BLK; ++t) {
+        const float x = (sP > 0.0f) ? Pt[t] / sP : 0.0f;
+        dq[t] = (double)nearbyintf((float)((double)x * (1.0 + delta))) - (double)nearbyintf((float)((double)x * (1.0 - delta)));
+      }
     for (int c = 0; c < d; ++c) {
       long long acc = 0; /* MM(P̂, V̂): exact */
       for (int t = 0; t < SB_BLK; ++t) {
@@ -127,25 +137,39 @@ static void sb_fwd_row(const int8_t* q, const int8_t* k, const int8_t* v, const 
         acc += (long long)Pq[t] * (long long)v[(size_t)key * d + c];
       }
       O[c] = alpha * O[c] + (double)acc * (double)sP * (double)sv[j0 / SB_BLK];
+      if (amb) {
+        double a = 0.0;
+        for (int t = 0; t < SB_BLK && j0 + t < Np; ++t) a += dq[t] * fabs((double)v[(size_t)(j0 + t) * d + c]);
+        amb[c] = alpha * amb[c] + a * (double)sP * (double)sv[j0 / SB_BLK];
+      }
     }
     m = m_new;
   }
   for (int c = 0; c < d; ++c) O[c] /= l;
+  if (amb)
+    for (int c = 0; c < d; ++c) amb[c] /= l;
   if (lse) *lse = scale * m + log(l);
 }
 
 /* Alg2 over a batch of BH heads (quantized by sb_quantize_head, stacked per head), rows[nrows] of each. */
-EXPORT void sb_attn_fwd(int BH, int N, int d, const int8_t* q, const int8_t* k, const int8_t* v, const float* sq,
-                        const float* sk, const float* sv, int causal, double scale, const int* rows, int nrows,
-                        double* O, double* lse) {
+EXPORT void sb_attn_fwd_amb(int BH, int N, int d, const int8_t* q, const int8_t* k, const int8_t* v,
+                            const float* sq, const float* sk, const float* sv, int causal, double scale, const int* rows,
+                            int nrows, double* O, double* lse, double delta, double* amb) {
   const int Np = (N + SB_BLK - 1) / SB_BLK * SB_BLK, T = Np / SB_BLK;
   for (int h = 0; h < BH; ++h) {
 #pragma omp parallel for schedule(dynamic, 1)
     for (int r = 0; r < nrows; ++r)
       sb_fwd_row(q + (size_t)h * Np * d, k + (size_t)h * Np * d, v + (size_t)h * Np * d, sq + (size_t)h * T,
                  sk + (size_t)h * T, sv + (size_t)h * T, N, Np, d, causal, rows[r], scale,
-                 &O[((size_t)h * nrows + r) * d], lse ? &lse[(size_t)h * nrows + r] : NULL);
+                 &O[((size_t)h * nrows + r) * d], lse ? &lse[(size_t)h * nrows + r] : NULL, delta,
+                 amb ? &amb[((size_t)h * nrows + r) * d] : NULL);
   }
+}
+
+EXPORT void sb_attn_fwd(int BH, int N, int d, const int8_t* q, const int8_t* k, const int8_t* v, const float* sq,
+                        const float* sk, const float* sv, int causal, double scale, const int* rows, int nrows,
+                        double* O, double* lse) {
+  sb_attn_fwd_amb(BH, N, d, q, k, v, sq, sk, sv, causal, scale, rows, nrows, O, lse, 0.0, NULL);
 }
 
 /* Alg3 for one head.  q, k int8 [Np][d] with sq, sk, km from sb_quantize_head; V16 = the 16-bit V values

@@ -53,13 +53,28 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_FUSED_P2
 #define SAGE3_FUSED_P2 0
 #endif
+#ifndef SAGE3_PV_CHUNK
+#define SAGE3_PV_CHUNK 16  // correction: PV_j columns per TMEM load
+#endif
+#ifndef SAGE3_PV_PIPE
+#define SAGE3_PV_PIPE 0  // 1: two PV loads in flight in the correction (chunk c+1 requested before chunk c's FFMA2s)
+#endif
+#ifndef SAGE3_XCHG_TMEM
+#define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
+#endif
+#ifndef SAGE3_PROD_BACKOFF
+#define SAGE3_PROD_BACKOFF 0  // 1: TMA producers poll their empty barriers with test_wait + timed sleep
+#endif
+__device__ __forceinline__ void prod_wait(uint64_t* bar, uint32_t parity) {
+#if SAGE3_PROD_BACKOFF
+  ptx::mbar_wait_backoff(bar, parity);
+#else
+  ptx::mbar_wait(bar, parity);
+#endif
+}
 constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
-#ifndef SAGE3_X_ARRIVALS
-#define SAGE3_X_ARRIVALS 128
-#endif
-constexpr int kXArrivals = SAGE3_X_ARRIVALS;  // x_full arrivals per tile: 128 (per thread) or 4 (per warp)
 constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
 constexpr int kThreads = 512;
 // Per-thread register budgets after setmaxnreg (one warp of each warpgroup per SM sub-partition:
@@ -85,6 +100,11 @@ constexpr uint32_t reg_correction() { return D == 64 ? SAGE3_REG_CORRECTION_D64 
 // S_j (MMA), then — once the softmax has read S_j — for PV_j (MMA), which the correction warpgroup reads
 // before the buffer is reused for S_{j+3}.  Scale factors in 32 more columns.
 constexpr int kSBufs = 3;
+// Softmax -> correction exchange of (exponent reference, rowsum(P̃2_j)) per row: two TMEM columns per slot in the
+// otherwise unused columns 416..431 (tile j -> slot j % 8).  The softmax warp writes its rows' pair with
+// tcgen05.st before its p_full arrival; the correction reads it after pv_full (the PV MMA of the same tile was
+// issued after p_full), so the hand-off needs no mbarrier of its own.
+constexpr uint32_t kColX = 416;
 
 template <int D, bool kMX>
 struct Layout {
@@ -148,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* b_empty = pv_full + kSBufs;   // correction -> MMA: buffer j%3 free again
   uint64_t* p_full = b_empty + kSBufs;    // softmax -> MMA: P̂2_j / s_P2 in smem buffer j%4, S_j consumed
   uint64_t* p_empty = p_full + kPBufs;    // MMA -> softmax: PV_j done with smem buffer j%4
-  uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8
+  uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8 (smem mode)
   uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (TMA)
   uint64_t* ds_empty = ds_full + kDsStages;  // softmax -> V producer: slot read
   uint64_t* m_full = ds_empty + kDsStages;    // direct P: m_j of tile j in xchg slot j%8 (softmax -> softmax)
@@ -184,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[b], 4);  // one arrival per softmax warp
       mbar_init(&p_empty[b], 1);
     }
-    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], kXArrivals);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 128);
     for (int s = 0; s < kXSlots; ++s) mbar_init(&m_full[s], 128);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
@@ -242,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = early ? SAGE3_EARLY_K : 0; j < nkv; ++j) {
           const int st = j % kKStages;
           const int row_k = bh * a.Np + j * 128;
-          mbar_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
+          prod_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
           tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
           bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
@@ -256,13 +276,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < nkv; ++j) {
           if constexpr (kSQ) {  // ds[bh][qt][128 j .. 128 j + 128): the GEMV term of this (query, key) tile
             const int ds_st = j % kDsStages;
-            mbar_wait(&ds_empty[ds_st], ((uint32_t)(j / kDsStages) & 1u) ^ 1u);
+            prod_wait(&ds_empty[ds_st], ((uint32_t)(j / kDsStages) & 1u) ^ 1u);
             mbar_arrive_expect_tx(&ds_full[ds_st], 512);
             bulk_load(smem + L::oDs + ds_st * 512, a.ds + ((int64_t)bh * n_qt + qt) * a.Np + j * 128, 512,
                       &ds_full[ds_st]);
           }
           const int st = j % kVStages;
-          mbar_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
+          prod_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
           tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
           bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
@@ -421,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait_regs(vb);
         tmem_ld_wait_regs(vc);
         tmem_ld_wait_regs(vd);
+        SAGE3_TRACE_EV(par ? 3 : 0, j, 1);
         pass1(0, va);
         pass1(1, vb);
         pass1(2, vc);
@@ -428,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
+      SAGE3_TRACE_EV(par ? 3 : 0, j, 2);
       const int slot = j % kXSlots;
       // the exponent reference of this tile's values: tmax_j (two-level: P̃2 = 2688·2^{sl2(S - tmax_j)}) or the
       // running max m_j (direct: P̃ = 2^{sl2(S - m_j)}); the correction warpgroup weights the tile by it
@@ -592,6 +614,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       sts_u32(sPSF, scw[0]);
       if constexpr (!kMX) sts_u32(sPSF + 512, scw[1]);
+#if SAGE3_XCHG_TMEM
+      {  // (eref, rowsum) -> the correction warpgroup through TMEM (lane = row), ordered by p_full -> PV -> pv_full
+        const uint32_t xv[2] = {__float_as_uint(eref), __float_as_uint(rowsum)};
+        tmem_st_32x32b_x2(lane_base + kColX + 2 * slot, xv);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      fence_proxy_async_smem();
+      // P̂2 / s_P2 (smem) and the TMEM exchange -> MMA: one arrival per warp after the warp's fences
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[pb]);
+#else
       if constexpr (!kDirect) sts_f32(xchg_s + slot * 1024, eref);
       sts_f32(xchg_s + slot * 1024 + 512, rowsum);
       tc_fence_before();
@@ -599,12 +633,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (tmax, rowsum) -> correction: every thread releases its own slot writes on x_full, so the hand-off is
       // ordered per thread (compute-sanitizer racecheck clean); P̂2 -> MMA: one arrival per warp after the
       // warp's proxy fences
-      if constexpr (kXArrivals == 128) mbar_arrive(&x_full[slot]);
+      mbar_arrive(&x_full[slot]);
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&p_full[pb]);
-        if constexpr (kXArrivals == 4) mbar_arrive(&x_full[slot]);
-      }
+      if (lane == 0) mbar_arrive(&p_full[pb]);
+#endif
       SAGE3_TRACE_WARP(1 + par, j, 4);
     };
     const int last = nkv - 1;
@@ -626,7 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = threadIdx.x - 128;
     const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-    const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
+    [[maybe_unused]] const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
     const float sl2 = a.scale * kLog2e;
     float mref = -INFINITY, l = 0.0f;
     f2 o[D / 2];
@@ -635,10 +667,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < nkv; ++j) {
       const int slot = j % kXSlots, b = j % kSBufs;
       SAGE3_TRACE_EV(4, j, 0);
+#if SAGE3_XCHG_TMEM
+      SAGE3_TRACE_EV(4, j, 1);
+      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
+      SAGE3_TRACE_EV(4, j, 2);
+      tc_fence_after();
+      uint32_t xv[2];
+      tmem_ld_32x32b_x2(lane_base + kColX + 2 * slot, xv);
+      tmem_ld_wait();
+      asm volatile("" : "+r"(xv[0]), "+r"(xv[1]));
+      const float tmax = __uint_as_float(xv[0]);
+      const float rs2 = __uint_as_float(xv[1]);
+#else
       mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
       SAGE3_TRACE_EV(4, j, 1);
       const float tmax = lds_f32(xchg_s + slot * 1024);
       const float rs2 = lds_f32(xchg_s + slot * 1024 + 512);
+#endif
       const bool need = (tmax - mref) * sl2 > 8.0f;  // true on the first tile (mref = -inf)
       if (__any_sync(0xffffffffu, need)) {
         const float mnew = need ? tmax : mref;
@@ -652,17 +697,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float w = ex2((tmax - mref) * sl2 - (kDirect ? 0.0f : kLog2_2688));  // tmax = the tile's eref
       l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
+#if !SAGE3_XCHG_TMEM
       mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
+#endif
+      constexpr int kPVC = SAGE3_PV_CHUNK;
+      const uint32_t pv_base = lane_base + 128 * b;
+      auto acc = [&](int c, const uint32_t(&v)[kPVC]) {
 #pragma unroll
-      for (int c = 0; c < D / 16; ++c) {
-        uint32_t v[16];
-        tmem_ld16(lane_base + 128 * b + 16 * c, v);
+        for (int i = 0; i < kPVC / 2; ++i)
+          o[kPVC / 2 * c + i] =
+              ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), ww, o[kPVC / 2 * c + i]);
+      };
+#if SAGE3_PV_PIPE
+      {  // PV_j in kPVC-column chunks, two in flight: chunk c+1 is requested before the FFMA2s of chunk c
+        uint32_t va[kPVC], vb[kPVC];
+        tmem_ld_cols(pv_base, va);
+        tmem_ld_wait_regs(va);
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          o[8 * c + i] = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), ww, o[8 * c + i]);
+        for (int c = 0; c < D / kPVC; c += 2) {
+          tmem_ld_cols(pv_base + kPVC * (c + 1), vb);
+          acc(c, va);
+          tmem_ld_wait_regs(vb);
+          if (c + 2 < D / kPVC) tmem_ld_cols(pv_base + kPVC * (c + 2), va);
+          acc(c + 1, vb);
+          if (c + 2 < D / kPVC) tmem_ld_wait_regs(va);
+        }
       }
+#else
+#pragma unroll
+      for (int c = 0; c < D / kPVC; ++c) {
+        uint32_t v[kPVC];
+        tmem_ld_cols(pv_base + kPVC * c, v);
+        tmem_ld_wait_regs(v);
+        acc(c, v);
+      }
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&b_empty[b]);

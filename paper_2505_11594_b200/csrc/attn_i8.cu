@@ -41,7 +41,7 @@ constexpr int kIThreads = 512;
 constexpr uint32_t kIRegWG0 = 32, kIRegSoftmax = 144, kIRegCorrection = 192;
 constexpr int kIMaxTiles = 1024;  // s_K, s_V of a head staged in smem: N_pad <= 128 K
 constexpr float kLog2_127 = 6.988684686772166f;
-constexpr uint32_t kMagicI = 0x4B400000u;  // float 1.5·2^23: int x + kMagicI reinterpreted = 12582912 + x exactly
+[[maybe_unused]] constexpr uint32_t kMagicI = 0x4B400000u;  // float 1.5·2^23: int x + kMagicI reinterpreted = 12582912 + x exactly
 constexpr float kMagicF = 12582912.0f;
 
 // kind::i8 instruction descriptor: D s32 ([4,6) = 2), A and B signed 8-bit ([7,10) = [10,13) = 1), K-major,

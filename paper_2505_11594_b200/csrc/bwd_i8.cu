@@ -49,7 +49,7 @@ using namespace ptx;
 constexpr int kBThreads = 512;
 constexpr uint32_t kBRegWG0 = 40, kBRegElem = 136, kBRegDV = 160, kBRegDK = 176;
 static_assert(kBRegWG0 + kBRegElem + kBRegDV + kBRegDK <= 512, "register budget");
-constexpr uint32_t kMagicIB = 0x4B400000u;  // float 1.5·2^23 bits: int x + kMagicIB reinterpreted = 12582912 + x
+[[maybe_unused]] constexpr uint32_t kMagicIB = 0x4B400000u;  // float 1.5·2^23 bits: int x + kMagicIB reinterpreted = 12582912 + x
 constexpr float kMagicFB = 12582912.0f;
 constexpr float kOne127B = 0x1.020408p-7f;  // fl32(1/127)
 constexpr int kDQBufs = 3;  // dQ staging buffers per WG3 warp

@@ -55,14 +55,53 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 // Blocking wait: try_wait with a suspend-time hint so waiting warps sleep in hardware instead of spinning
 // through issue slots shared with the compute warps.
+#ifndef SAGE3_WAIT_MODE
+#define SAGE3_WAIT_MODE 0
+#endif
+#ifndef SAGE3_WAIT_HINT
+#define SAGE3_WAIT_HINT 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SAGE3_WAIT_MODE == 1
+  // no suspend-time hint: the hardware's default try_wait time limit
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra.uni WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity), "r"((uint32_t)SAGE3_WAIT_HINT)
       : "memory");
+#endif
+}
+
+// Non-blocking probe of the phase.
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait for producers whose refill latency is hidden by a deep ring (TMA loads): probe, then a plain timed sleep
+// between probes.  Unlike the try_wait suspend (NANOSLEEP.SYNCS, woken by every mbarrier event of the CTA), this
+// neither wakes on unrelated arrivals nor keeps SYNCS operations in the MIO queue that MUFU shares.
+#ifndef SAGE3_PROD_SLEEP_NS
+#define SAGE3_PROD_SLEEP_NS 128
+#endif
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) __nanosleep(SAGE3_PROD_SLEEP_NS);
 }
 
 // ---------------------------------------------------------------- proxy fences
@@ -214,6 +253,12 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
+}
+__device__ __forceinline__ void tmem_ld_32x32b_x2(uint32_t taddr, uint32_t (&r)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_32x32b_x2(uint32_t taddr, const uint32_t (&r)[2]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(r[0]), "r"(r[1]) : "memory");
 }
 __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(

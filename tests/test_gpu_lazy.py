@@ -10,14 +10,15 @@ import torch
 import oracle
 import paper_2505_11594_b200 as s3
 import synth
-from test_gpu_attn import check, oracle_heads
+from parity import check, oracle_attention
+from test_gpu_attn import oracle_heads
 
 pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("fmt", ["nvfp4", "mxfp4"])
 @pytest.mark.parametrize("causal", [False, True])
-@pytest.mark.parametrize("N,d", [(128, 128), (300, 64), (1024, 128), (2500, 64)])
+@pytest.mark.parametrize("N,d", [(1, 64), (15, 128), (127, 64), (128, 128), (300, 64), (1024, 128), (2500, 64)])
 def test_lazy_parity(N, d, causal, fmt):
     B, H = 1, 2
     Q, K, V = synth.make_qkv(B, H, N, d, seed=17 * N + d, dtype=torch.bfloat16, device="cuda")
@@ -26,10 +27,10 @@ def test_lazy_parity(N, d, causal, fmt):
     O = s3.sage3_attn_fwd(qkv, causal=causal, out_dtype=torch.float32, lse=lse, p_quant="lazy")
     torch.cuda.synchronize()
     rows = np.arange(N, dtype=np.int32) if N <= 1024 else np.arange(0, N, 7, dtype=np.int32)
-    ref, ref_lse = oracle.attn_fwd(oracle_heads(qkv, range(B * H)), causal=causal, scale=1 / math.sqrt(d),
-                                   p_mode=oracle.PMODE_LAZY, want_lse=True, rows=rows)
+    ref, ref_lse, amb, vmax = oracle_attention(oracle_heads(qkv, range(B * H)), causal=causal,
+                                               scale=1 / math.sqrt(d), p_mode=oracle.PMODE_LAZY, rows=rows)
     for bh in range(B * H):
-        check(O[0, bh].cpu().numpy()[rows], ref[bh], torch.float32, f"head {bh}")
+        check(O[0, bh].cpu().numpy()[rows], ref[bh], torch.float32, f"head {bh}", amb=amb[bh], vmax=vmax[bh])
     np.testing.assert_allclose(lse.cpu().numpy().reshape(B * H, N)[:, rows], ref_lse, rtol=1e-5, atol=1e-4)
     O2 = torch.zeros_like(O)
     n = s3.n_units(qkv)

@@ -13,11 +13,10 @@ import oracle
 import paper_2505_11594_b200 as s3
 import synth
 from layout import decode_head
+from parity import check, oracle_attention
 
 pytestmark = pytest.mark.gpu
 
-REL_L1_MAX = 2e-3
-COS_MIN = 0.9999
 MX = oracle.FMT_MXFP4
 
 
@@ -86,18 +85,11 @@ def oracle_heads(qkv, heads):
     return out
 
 
-def check(gpu, ref, dtype, what=""):
-    r = torch.from_numpy(ref).to(dtype).double().numpy()
-    g = gpu.astype(np.float64)
-    assert np.all(np.isfinite(g)), what
-    m = oracle.accuracy_metrics(r, g)
-    assert m["l1"] <= REL_L1_MAX and m["cos_sim"] >= COS_MIN, f"{what}: {m}"
-    return m
 
 
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("d", [64, 128])
-@pytest.mark.parametrize("N", [128, 300, 1024])
+@pytest.mark.parametrize("N", [1, 31, 127, 128, 300, 1024])
 def test_mxfp4_attention_parity(N, d, causal):
     B, H = 1, 2
     Q, K, V = synth.make_qkv(B, H, N, d, seed=5 * N + d, dtype=torch.bfloat16, device="cuda")
@@ -105,10 +97,10 @@ def test_mxfp4_attention_parity(N, d, causal):
     lse = torch.empty(B, H, N, dtype=torch.float32, device="cuda")
     O = s3.sage3_attn_fwd(qkv, causal=causal, lse=lse, out_dtype=torch.float32)
     torch.cuda.synchronize()
-    ref, ref_lse = oracle.attn_fwd(oracle_heads(qkv, range(B * H)), causal=causal, scale=1 / math.sqrt(d),
-                                   want_lse=True)
+    ref, ref_lse, amb, vmax = oracle_attention(oracle_heads(qkv, range(B * H)), causal=causal,
+                                               scale=1 / math.sqrt(d))
     for bh in range(B * H):
-        check(O[0, bh].cpu().numpy(), ref[bh], torch.float32, f"head {bh}")
+        check(O[0, bh].cpu().numpy(), ref[bh], torch.float32, f"head {bh}", amb=amb[bh], vmax=vmax[bh])
     np.testing.assert_allclose(lse.cpu().numpy().reshape(B * H, N), ref_lse, rtol=1e-5, atol=1e-4)
 
 
@@ -144,9 +136,9 @@ def test_mxfp4_smooth_q_and_units():
     heads = [oracle.quantize_head(*(x[0, bh].float().cpu().numpy() for x in (Q, K, V)), smooth_q=True, fmt=MX)
              for bh in range(3)]
     rows = np.arange(0, N, 3, dtype=np.int32)
-    ref = oracle.attn_fwd(heads, causal=True, scale=1 / math.sqrt(d), rows=rows)
+    ref, _, amb, vmax = oracle_attention(heads, causal=True, scale=1 / math.sqrt(d), rows=rows)
     for bh in range(3):
-        check(O[0, bh].cpu().numpy()[rows], ref[bh], torch.float32, f"head {bh}")
+        check(O[0, bh].cpu().numpy()[rows], ref[bh], torch.float32, f"head {bh}", amb=amb[bh], vmax=vmax[bh])
 
 
 def test_nvfp4_more_accurate_than_mxfp4_on_gpu():

@@ -9,6 +9,7 @@ import torch
 
 import oracle
 import paper_2505_11594_b200 as s3
+import parity
 import synth
 
 pytestmark = pytest.mark.gpu
@@ -41,13 +42,19 @@ def test_int8_quantize_bit_exact(dtype, d, N):
             assert bad.size == 0, f"{name}: {len(bad)} mismatches, first {bad[:3].tolist()}"
 
 
-def check(gpu, ref, what=""):
-    m = oracle.accuracy_metrics(ref, gpu.astype(np.float64))
-    assert np.all(np.isfinite(gpu)) and m["l1"] <= 2e-3 and m["cos_sim"] >= 0.9999, f"{what}: {m}"
+def check(gpu, ref, what="", amb=None, vmax=None):
+    """north_star per-head gate + the element-wise bound of tests/parity.py (fp32 output)."""
+    return parity.check(gpu, ref, torch.float32, what, amb=amb, vmax=vmax)
+
+
+def sb_vmax(h) -> float:
+    """max |deq(V̂)| of a SageBwd head: |int8 code| x its block scale."""
+    T = h.Np // 128
+    return float((np.abs(h.v.astype(np.float64)).reshape(T, 128, -1).max(axis=(1, 2)) * h.sv).max())
 
 
 @pytest.mark.parametrize("causal", [False, True])
-@pytest.mark.parametrize("N,d", [(128, 128), (300, 64), (1000, 128), (2000, 64)])
+@pytest.mark.parametrize("N,d", [(1, 64), (15, 128), (127, 64), (128, 128), (300, 64), (1000, 128), (2000, 64)])
 def test_int8_attention_parity(N, d, causal):
     B, H = 1, 2
     Q, K, V = synth.make_qkv(B, H, N, d, seed=N + d, dtype=torch.bfloat16, device="cuda", outliers=False)
@@ -56,10 +63,11 @@ def test_int8_attention_parity(N, d, causal):
     O = s3.sage3_int8_attn_fwd(qkv, causal=causal, lse=lse, out_dtype=torch.float32)
     torch.cuda.synchronize()
     rows = np.arange(N, dtype=np.int32) if N <= 1000 else np.arange(0, N, 3, dtype=np.int32)
-    ref, ref_lse = oracle.sb_attn_fwd([decode(qkv, bh) for bh in range(B * H)], causal=causal,
-                                      scale=1 / math.sqrt(d), rows=rows, want_lse=True)
+    heads = [decode(qkv, bh) for bh in range(B * H)]
+    ref, ref_lse, amb = oracle.sb_attn_fwd(heads, causal=causal, scale=1 / math.sqrt(d), rows=rows,
+                                           amb_delta=parity.AMB_DELTA)
     for bh in range(B * H):
-        check(O[0, bh].cpu().numpy()[rows], ref[bh], f"head {bh}")
+        check(O[0, bh].cpu().numpy()[rows], ref[bh], f"head {bh}", amb=amb[bh], vmax=sb_vmax(heads[bh]))
     np.testing.assert_allclose(lse.cpu().numpy().reshape(B * H, N)[:, rows], ref_lse, rtol=1e-5, atol=1e-4)
 
 

@@ -41,10 +41,23 @@ def _case(B, H, N, d, causal, seed, dtype=torch.bfloat16, outliers=True):
     return Q, K, V, dO, O.cuda(), L.cuda().contiguous(), qkv, refs, scale
 
 
+ROW_L1_MAX = 2e-2
+
+
 def _check(got, ref, what):
+    """north_star per-head gate, plus a per-row bound: every gradient row (a query row of dQ, a key row of dK/dV)
+    has an L1 error within ROW_L1_MAX of the head's MEAN row L1 norm, so one wrong row or tile cannot hide inside
+    the head average.  (Relative to the row's own norm would not do: ψ(dS) has one INT8 scale per 128 x 128 tile,
+    so rows of small dS carry few quantization levels and a single code decided differently at a rounding
+    midpoint moves them by percents of their own size.)"""
     m = oracle.accuracy_metrics(ref, got.astype(np.float64))
     assert np.all(np.isfinite(got)), what
     assert m["l1"] <= 2e-3 and m["cos_sim"] >= 0.9999, f"{what}: {m}"
+    g = got.astype(np.float64)
+    row = np.abs(g - ref).sum(axis=1) / (np.abs(ref).sum(axis=1).mean() + 1e-300)
+    bad = np.argwhere(row > ROW_L1_MAX)
+    assert bad.size == 0, f"{what}: rows {bad[:5, 0].tolist()} L1 / mean row L1 {row[bad[:5, 0]].tolist()}"
+    m["max_row_l1"] = float(row.max())
     return m
 
 

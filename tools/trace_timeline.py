@@ -53,8 +53,9 @@ for cta in range(2):
     print(f" latency S-issue->softmax wake {np.mean(lat_s) if lat_s else 0:6.0f} (n={len(lat_s)})"
           f"  PV-issue->correction wake {np.mean(lat_pv) if lat_pv else 0:6.0f} (n={len(lat_pv)})"
           f"  b_empty->S issue {np.mean(lat_b) if lat_b else 0:6.0f} (n={len(lat_b)})")
-    tot = t[4, nkv - 1, 3] - t0
-    print(f" CTA span {tot} cycles for {nkv} tiles = {tot / nkv:.0f} cycles/tile")
+    nl = min(nkv, 128)
+    tot = t[4, nl - 1, 3] - t0
+    print(f" CTA span {tot} cycles for {nl} tiles = {tot / nl:.0f} cycles/tile")
     for j in (10, 11, 12):
         print(f"  tile {j}: S issued {t[5,j,3]-t0}, softmax start {t[1+j%2,j,1]-t0}, P ready {t[1+j%2,j,4]-t0},"
               f" PV issued {t[6,j,3]-t0}, corr pv-wake {t[4,j,2]-t0}, corr done {t[4,j,3]-t0}")
@@ -73,7 +74,7 @@ for j in range(8, 20):
     w0 = t[sm, j, 1]
     print(f" tile {j:2d} WG{sm-1}: " + " ".join(f"{int(t[sm, j, 4 + w] - w0):6d}" for w in range(4)))
 
-print("\nsoftmax sub-events (relative to the warpgroup's S wake k1): ld01-wait, pass1a, ld23-wait, pass1b(tmax), scales, pass2-ld0-wait, pass2-ld3-wait, P ready")
+print("\nsoftmax sub-events (relative to the warpgroup's S wake k1): -, S loads waited, tmax, -, scales done, pass2-ld0-wait, pass2-ld3-wait, P ready")
 for j in range(8, 20):
     sm = 1 + j % 2
     sub = 0 if sm == 1 else 3
