@@ -152,9 +152,13 @@ sage3_status sage3_attn_fwd_units(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sag
 typedef enum {
   SAGE3_P_TWO_LEVEL = 0, /* the method: s_P1 = rowmax(P̃)/(448·6), P̂2 = φ(P̃/s_P1) (§3.2, Alg1 L10)   */
   SAGE3_P_DIRECT = 1,    /* ablation (Tab1b): P̂ = φ(P̃), P̃ = exp(scale(S - m_j)) with the running max */
-  SAGE3_P_TWO_LEVEL_LAZY = 2 /* throughput variant (reading n1): the first level
+  SAGE3_P_TWO_LEVEL_LAZY = 2, /* throughput variant (reading n1): the first level
                               * is a per-row reference r moved to the tile max only when that exceeds r by more
                               * than 2^8 in weight; P̂2 = φ(10.5·exp(scale(S - r))); O accumulates in TMEM      */
+  SAGE3_P_TWO_LEVEL_QSUM = 3 /* throughput variant (reading n2): P̂2 exactly as
+                              * TWO_LEVEL, but the row sum l of Alg1 L9 accumulates the QUANTIZED P (s_P1·Σ deq(P̂2),
+                              * read from the tensor core: P̂2 times a ones column) instead of the unquantized P̃
+                              * (reading c9).  NVFP4 only (MXFP4: SAGE3_ERR_UNSUPPORTED).                        */
 } sage3_p_quant;
 typedef struct {
   int32_t causal;       /* != 0: key j visible to query i iff j <= i                                      */

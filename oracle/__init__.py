@@ -30,7 +30,7 @@ _CFLAGS = ["-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fopenmp",
 _lock = threading.Lock()
 _lib = None
 
-PMODE_TWO_LEVEL, PMODE_DIRECT, PMODE_NONE, PMODE_LAZY = 0, 1, 2, 3  # LAZY: NEXT #2 variant (reading n1)
+PMODE_TWO_LEVEL, PMODE_DIRECT, PMODE_NONE, PMODE_LAZY, PMODE_QSUM = 0, 1, 2, 3, 4  # LAZY, QSUM: NEXT #2 variants (readings n1, n2)
 
 
 def build(force: bool = False) -> str:

@@ -328,6 +328,10 @@ EXPORT void oracle_fp4mm(const uint8_t* a_codes, const uint8_t* a_sf, const uint
 #define PMODE_DIRECT 1
 #define PMODE_NONE 2
 #define PMODE_LAZY 3 /* NEXT #2 throughput variant (not the paper's Alg1 L10): see attn_row_lazy */
+#define PMODE_QSUM 4 /* NEXT #2 throughput variant (not the paper's Alg1 L9): two-level P exactly as Alg1 L10, but
+                      * the row sum l accumulates the QUANTIZED P (s_P1 · Σ deq(P̂2)), which the GPU obtains from
+                      * the tensor core (P̂2 times a ones column) instead of summing the unquantized P̃ (reading c9).
+                      * O/l is then the normalised average of V with exactly the weights the PV product used. */
 
 EXPORT float oracle_two_level_row_fmt(const float* P, int n, int p_mode, int fmt, uint8_t* codes, uint8_t* sf) {
   const int G = fmt ? 32 : 16;
@@ -348,7 +352,7 @@ EXPORT float oracle_two_level_row_fmt(const float* P, int n, int p_mode, int fmt
     memset(sf, 0, (size_t)n / G);
     return 0.0f;
   }
-  for (int b = 0; b < n; b += G) {
+  for (int b = 0; b < n; b += G) { /* (PMODE_QSUM quantizes exactly as the two-level mode) */
     for (int i = 0; i < G; ++i) p2[i] = P[b + i] / sP1;
     if (fmt) oracle_phi_mxfp4(p2, &codes[b], &sf[b / G]);
     else oracle_phi_nvfp4(p2, &codes[b], &sf[b / G]);
@@ -517,6 +521,7 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
   uint8_t* pc = (uint8_t*)malloc((size_t)Bkv);
   uint8_t* ps = (uint8_t*)malloc((size_t)Bkv / 16 + 1);
   double* dq = amb ? (double*)malloc(sizeof(double) * (size_t)Bkv) : NULL;
+  double ambs = 0.0; /* PMODE_QSUM: decision sensitivity of l */
   float p2[32];
   for (int c = 0; c < d; ++c) O[c] = 0.0;
   if (amb)
@@ -551,7 +556,7 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
       Pq[t] = e;        /* kept in fp64 only by the unquantized pin mode (p_mode NONE) */
       rowsum += (p_mode == PMODE_NONE) ? e : (double)Pt[t];
     }
-    l = alpha * l + rowsum;
+    if (p_mode != PMODE_QSUM) l = alpha * l + rowsum; /* (PMODE_QSUM: after the quantization below) */
     /* Alg1 L10: two-level quantization of P̃ (or the ablation modes) */
     double sP1;
     if (p_mode == PMODE_NONE) {
@@ -565,6 +570,16 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
           for (int i = 0; i < G; ++i) p2[i] = p_mode == PMODE_DIRECT ? Pt[b + i] : Pt[b + i] / (float)sP1;
           oracle_phi_sensitivity(p2, G, fmt, delta, &dq[b]);
         }
+      if (p_mode == PMODE_QSUM) { /* l from the quantized P: s_P1 · Σ deq(P̂2) */
+        double qs = 0.0;
+        for (int t = 0; t < Bkv; ++t) qs += Pq[t];
+        l = alpha * l + qs * sP1;
+        if (amb) { /* a decision moves the denominator too: its share is applied with |O| at the end */
+          double a = 0.0;
+          for (int t = 0; t < Bkv; ++t) a += dq[t];
+          ambs = alpha * ambs + a * sP1;
+        }
+      }
     }
     /* Alg1 L11: O = diag(alpha) O + FP4MM(P̂2, s_P2, V̂, s_V) * s_P1 (inner sum exact in fp64) */
     for (int c = 0; c < d; ++c) {
@@ -589,7 +604,7 @@ static void attn_row(const double* Qrow, const double* Kd, const double* Vt, int
   /* Alg1 L13: O_i = diag(l)^-1 O */
   for (int c = 0; c < d; ++c) O[c] /= l;
   if (amb)
-    for (int c = 0; c < d; ++c) amb[c] /= l;
+    for (int c = 0; c < d; ++c) amb[c] = amb[c] / l + ambs / l * fabs(O[c]);
   if (lse) *lse = scale * m + log(l);
   free(dq);
   free(S);

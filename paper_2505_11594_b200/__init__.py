@@ -21,8 +21,9 @@ SAGE3_FP16, SAGE3_BF16, SAGE3_FP32 = 0, 1, 2
 SAGE3_NVFP4, SAGE3_MXFP4 = 0, 1  # sage3_fp4_format: the method / the Tab1a data-type ablation
 _FMT = {"nvfp4": SAGE3_NVFP4, "mxfp4": SAGE3_MXFP4, SAGE3_NVFP4: SAGE3_NVFP4, SAGE3_MXFP4: SAGE3_MXFP4}
 # sage3_p_quant: the method / the Tab1b ablation / the NEXT #2 lazy-reference throughput variant
-SAGE3_P_TWO_LEVEL, SAGE3_P_DIRECT, SAGE3_P_TWO_LEVEL_LAZY = 0, 1, 2
-_PQ = {"two_level": SAGE3_P_TWO_LEVEL, "direct": SAGE3_P_DIRECT, "lazy": SAGE3_P_TWO_LEVEL_LAZY}
+SAGE3_P_TWO_LEVEL, SAGE3_P_DIRECT, SAGE3_P_TWO_LEVEL_LAZY, SAGE3_P_TWO_LEVEL_QSUM = 0, 1, 2, 3
+_PQ = {"two_level": SAGE3_P_TWO_LEVEL, "direct": SAGE3_P_DIRECT, "lazy": SAGE3_P_TWO_LEVEL_LAZY,
+       "qsum": SAGE3_P_TWO_LEVEL_QSUM}
 _DT = {torch.float16: SAGE3_FP16, torch.bfloat16: SAGE3_BF16, torch.float32: SAGE3_FP32}
 
 # Every function include/sage3.h declares (checked by tests/test_abi.py).

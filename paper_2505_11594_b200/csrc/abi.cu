@@ -160,9 +160,10 @@ sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_
                                const sage3_attn_options* opts, float* lse, void* stream) {
   if (!qkv || !opts || !shape_ok(qkv->B, qkv->H, qkv->N, qkv->d)) return SAGE3_ERR_INVALID_ARG;
   if ((opts->p_quant != SAGE3_P_TWO_LEVEL && opts->p_quant != SAGE3_P_DIRECT &&
-       opts->p_quant != SAGE3_P_TWO_LEVEL_LAZY) ||
+       opts->p_quant != SAGE3_P_TWO_LEVEL_LAZY && opts->p_quant != SAGE3_P_TWO_LEVEL_QSUM) ||
       opts->reserved != 0)
     return SAGE3_ERR_INVALID_ARG;
+  if (opts->p_quant == SAGE3_P_TWO_LEVEL_QSUM && qkv->fmt != SAGE3_NVFP4) return SAGE3_ERR_UNSUPPORTED;
   if (opts->p_quant != SAGE3_P_TWO_LEVEL && (qkv->q_mean || qkv->ds)) return SAGE3_ERR_INVALID_ARG;
   const int causal = opts->causal;
   const float softmax_scale = opts->softmax_scale;
@@ -189,6 +190,7 @@ sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_
   a.ds = qkv->ds;
   a.mx = qkv->fmt == SAGE3_MXFP4;
   a.p_direct = opts->p_quant == SAGE3_P_DIRECT;
+  a.p_qsum = opts->p_quant == SAGE3_P_TWO_LEVEL_QSUM;
   a.q_data = qkv->q_data, a.k_data = qkv->k_data, a.v_data = qkv->v_data;
   a.q_sf = qkv->q_sf, a.k_sf = qkv->k_sf, a.v_sf = qkv->v_sf;
   a.o = o.ptr, a.o_sb = o.stride_b, a.o_sh = o.stride_h, a.o_sn = o.stride_n, a.o_dtype = (int)o_dtype;

@@ -50,9 +50,6 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_EARLY_K
 #define SAGE3_EARLY_K 1  // K tiles requested in the prologue (<= kKStages)
 #endif
-#ifndef SAGE3_FUSED_P2
-#define SAGE3_FUSED_P2 0
-#endif
 #ifndef SAGE3_PV_CHUNK
 #define SAGE3_PV_CHUNK 16  // correction: PV_j columns per TMEM load
 #endif
@@ -105,8 +102,12 @@ constexpr int kSBufs = 3;
 // tcgen05.st before its p_full arrival; the correction reads it after pv_full (the PV MMA of the same tile was
 // issued after p_full), so the hand-off needs no mbarrier of its own.
 constexpr uint32_t kColX = 416;
+// Row-sum variant (kQSum, p_quant = SAGE3_P_TWO_LEVEL_QSUM, reading n2): l accumulates the quantized P,
+// computed by the tensor core as P̂2 (M=128, K=128) times a 16-column all-ones FP4 matrix (scales 1.0) into 16
+// TMEM columns per S/PV buffer (tile j -> kColRS + 16 (j % 3)); the ones operand's scale factors sit at kColSF1.
+constexpr uint32_t kColSF1 = 432, kColRS = 448;
 
-template <int D, bool kMX>
+template <int D, bool kMX, bool kQSum = false>
 struct Layout {
   static constexpr int kQKRow = D / 2;          // bytes per Q/K row (64 or 32)
   static constexpr int kQBytes = 128 * kQKRow;   // Q tile codes
@@ -129,7 +130,10 @@ struct Layout {
   static constexpr int oPSF = oVSF + kVStages * kVSF;
   static constexpr int oXchg = oPSF + kPBufs * kPSF;            // float [kXSlots][2][128]: tmax_j, rowsum(P̃2_j)
   static constexpr int oDs = oXchg + kXSlots * 2 * 128 * 4;  // smoothing Q: ds rows of 128 keys, kDsStages slots
-  static constexpr int oBar = oDs + kDsStages * 512;
+  // kQSum: the all-ones B operand (16 rows x 128 keys, E2M1 1.0 = code 2 in every nibble) and its SF atoms (E4M3 1.0)
+  static constexpr int oOnes = ((oDs + kDsStages * 512 + 1023) / 1024) * 1024;
+  static constexpr int oOnesSF = oOnes + 1024;
+  static constexpr int oBar = kQSum ? oOnesSF + 1024 : oDs + kDsStages * 512;
   static constexpr int kNumBars =
       1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages;
   static constexpr int oTmem = oBar + kNumBars * 8;
@@ -144,12 +148,12 @@ struct Layout {
 // RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
 // of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
 // warpgroups are no longer independent in this mode.
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                     const AttnArgs a) {
-  using L = Layout<D, kMX>;
+  using L = Layout<D, kMX, kQSum>;
   extern __shared__ uint8_t smem_raw[];
   // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
   __shared__ __align__(1024) float2 s_lut[128];
@@ -239,6 +243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // multiplied by s = 0 in the MMA, reading c5), its row-sum contribution is Σy·2^-10.
     const bool zero = (s == 0.0f || c == 0x7F);
     s_lut[c] = make_float2(zero ? 10.0f : -log2f(s), zero ? 0x1p-10f : s);
+  }
+  if constexpr (kQSum) {  // the constant ones operand and its scales (generic stores -> async proxy before the sync)
+    uint32_t* ones = reinterpret_cast<uint32_t*>(smem + L::oOnes);
+    for (int i = threadIdx.x; i < 512; i += kThreads) ones[i] = i < 256 ? 0x22222222u : 0x38383838u;
+    fence_proxy_async_smem();
   }
   tc_fence_before();
   __syncthreads();
@@ -350,6 +359,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = make_smem_desc(smem_u32(sV) + 32 * ks, 16, 512, kLayoutSw64);
             mma(tbase + 128 * b, ad, bd, D, ks, tbase + kColSFP, tbase + kColSFV);
           }
+          if constexpr (kQSum) {  // row sums of the quantized P̂2: P̂2 x ones (N = 16)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint64_t ad = make_smem_desc(smem_u32(sP) + 32 * ks, 16, 512, kLayoutSw64);
+              const uint64_t bd = make_smem_desc(smem_u32(smem + L::oOnes) + 32 * ks, 16, 512, kLayoutSw64);
+              mma_nvf4(tbase + kColRS + 16 * b, ad, bd, make_idesc_nvf4(128, 16), tbase + kColSFP + 4 * ks,
+                       tbase + kColSF1 + 4 * ks, ks > 0);
+            }
+          }
           mma_commit(&v_empty[st]);
           mma_commit(&p_empty[pb]);
           mma_commit(&pv_full[b]);
@@ -362,6 +380,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * at, sf_desc(sQSF + 512 * at));
           for (int j = 0; j < nkv; ++j) issue_s(j);  // S_j into buffer j%3 once the correction freed it
         } else {
+          if constexpr (kQSum) {
+#pragma unroll
+            for (int at = 0; at < 2; ++at)
+              tmem_cp_32x128b_x4(tbase + kColSF1 + 4 * at, sf_desc(smem + L::oOnesSF + 512 * at));
+          }
           for (int j = 0; j < nkv; ++j) issue_pv(j);
         }
       }
@@ -536,61 +559,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int hb = 0; hb < 2; ++hb) {
           const f2* yy = y + 8 * hb;
-          const f2 s01 = fadd2(fadd2(yy[0], yy[1]), fadd2(yy[2], yy[3]));
-          const f2 s23 = fadd2(fadd2(yy[4], yy[5]), fadd2(yy[6], yy[7]));
-          const f2 sy = fadd2(s01, s23);
-          rowsum = fmaf(hb ? sB : sA, sy.x + sy.y, rowsum);
+          if constexpr (!kQSum) {  // (kQSum: the row sum comes from the tensor core)
+            const f2 s01 = fadd2(fadd2(yy[0], yy[1]), fadd2(yy[2], yy[3]));
+            const f2 s23 = fadd2(fadd2(yy[4], yy[5]), fadd2(yy[6], yy[7]));
+            const f2 sy = fadd2(s01, s23);
+            rowsum = fmaf(hb ? sB : sA, sy.x + sy.y, rowsum);
+          }
           w[2 * hb] = cvt_e2m1x8(yy[0].x, yy[0].y, yy[1].x, yy[1].y, yy[2].x, yy[2].y, yy[3].x, yy[3].y);
           w[2 * hb + 1] = cvt_e2m1x8(yy[4].x, yy[4].y, yy[5].x, yy[5].y, yy[6].x, yy[6].y, yy[7].x, yy[7].y);
         }
         // 16-byte chunk c = keys [32c, 32c+32) of row r, SWIZZLE_64B (chunk ^= (row>>1)&3)
         sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
       };
-#if SAGE3_FUSED_P2
-      // exps of chunk c and the finish of chunk c-1 fused quarter by quarter (4 pairs of exps, then one E2M1
-      // word and one partial row sum of the previous chunk), spreading the MUFU issue between FMA/ALU work;
-      // the same operations in the same tree order as exps + finish (bitwise identical results).
-      auto step = [&](int c, const uint32_t(&v)[32], f2(&y)[16], int cp, const f2(&yp)[16]) {
-        const float nA = c == 1 ? nbb[2] : c == 2 ? nbb[4] : nbb[6];
-        const float nB = c == 1 ? nbb[3] : c == 2 ? nbb[5] : nbb[7];
-        const float sA = cp == 0 ? sdec[0] : cp == 1 ? sdec[2] : sdec[4];
-        const float sB = cp == 0 ? sdec[1] : cp == 1 ? sdec[3] : sdec[5];
-        uint32_t w[4];
-        f2 qs[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-#pragma unroll
-          for (int i = 4 * q; i < 4 * q + 4; ++i) {
-            const float nbh = i < 8 ? nA : nB;
-            const f2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2,
-                               make_float2(nbh, nbh));
-            y[i] = ((kPolyMask >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          }
-          const f2* yy = yp + 4 * q;
-          qs[q] = fadd2(fadd2(yy[0], yy[1]), fadd2(yy[2], yy[3]));
-          w[q] = cvt_e2m1x8(yy[0].x, yy[0].y, yy[1].x, yy[1].y, yy[2].x, yy[2].y, yy[3].x, yy[3].y);
-        }
-        const f2 syA = fadd2(qs[0], qs[1]), syB = fadd2(qs[2], qs[3]);
-        rowsum = fmaf(sA, syA.x + syA.y, rowsum);
-        rowsum = fmaf(sB, syB.x + syB.y, rowsum);
-        sts_v4(sP + ((cp ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
-      };
-      {
-        f2 ya[16], yb[16];
-        tmem_ld_wait_regs(va);
-        tmem_ld_32x32b_x32(s_addr + 32, vb);
-        exps(0, va, ya);
-        tmem_ld_wait_regs(vb);
-        tmem_ld_32x32b_x32(s_addr + 64, va);
-        step(1, vb, yb, 0, ya);
-        tmem_ld_wait_regs(va);
-        tmem_ld_32x32b_x32(s_addr + 96, vb);
-        step(2, va, ya, 1, yb);
-        tmem_ld_wait_regs(vb);
-        step(3, vb, yb, 2, ya);
-        finish(3, yb);
-      }
-#else
       {
         f2 ya[16], yb[16];
         tmem_ld_wait_regs(va);
@@ -611,7 +591,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         finish(2, ya);
         finish(3, yb);
       }
-#endif
       sts_u32(sPSF, scw[0]);
       if constexpr (!kMX) sts_u32(sPSF + 512, scw[1]);
 #if SAGE3_XCHG_TMEM
@@ -695,13 +674,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         mref = mnew;
       }
       const float w = ex2((tmax - mref) * sl2 - (kDirect ? 0.0f : kLog2_2688));  // tmax = the tile's eref
-      l = fmaf(w, rs2, l);
+      if constexpr (!kQSum) l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
 #if !SAGE3_XCHG_TMEM
       mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
 #endif
+      if constexpr (kQSum) {  // l += w · Σ deq(P̂2) of this tile, from the tensor core's ones-column product
+        uint32_t rq[1];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rq[0]) : "r"(lane_base + kColRS + 16 * b));
+        tmem_ld_wait();
+        asm volatile("" : "+r"(rq[0]));
+        l = fmaf(w, __uint_as_float(rq[0]), l);
+      }
       constexpr int kPVC = SAGE3_PV_CHUNK;
       const uint32_t pv_base = lane_base + 128 * b;
       auto acc = [&](int c, const uint32_t(&v)[kPVC]) {
@@ -768,14 +754,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------- host
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
 cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D, kMX>;
+  using L = Layout<D, kMX, kQSum>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
@@ -788,16 +774,16 @@ cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
+  attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
   return cudaGetLastError();
 }
 
-template <int D, bool kSQ, bool kMX, bool kDirect>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kQSum = false>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
   if constexpr (!kSQ && !kDirect) {  // the north_star path: long sequences take the early-TMA instantiation
-    if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true>(a, stream);
+    if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true, kQSum>(a, stream);
   }
-  return launch_dk<D, kSQ, kMX, kDirect, false>(a, stream);
+  return launch_dk<D, kSQ, kMX, kDirect, false, kQSum>(a, stream);
 }
 
 }  // namespace
@@ -806,6 +792,11 @@ template <bool kMX>
 cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
   if (a.p_direct) {  // ablation: no smoothing-Q instantiation (rejected in abi.cu)
     return a.d == 128 ? launch_d<128, false, kMX, true>(a, stream) : launch_d<64, false, kMX, true>(a, stream);
+  }
+  if constexpr (!kMX) {  // NEXT #2 row-sum variant (NVFP4 only, no smoothing Q: rejected in abi.cu)
+    if (a.p_qsum)
+      return a.d == 128 ? launch_d<128, false, false, false, true>(a, stream)
+                        : launch_d<64, false, false, false, true>(a, stream);
   }
   if (a.ds) return a.d == 128 ? launch_d<128, true, kMX, false>(a, stream) : launch_d<64, true, kMX, false>(a, stream);
   return a.d == 128 ? launch_d<128, false, kMX, false>(a, stream) : launch_d<64, false, kMX, false>(a, stream);

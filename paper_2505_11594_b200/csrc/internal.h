@@ -90,6 +90,7 @@ struct AttnArgs {
   const float* ds;  // smoothing Q (nullable): [B][H][Np/128][Np], added to S
   bool mx;          // MXFP4 operands (scale_vec::2X MMAs, 32-key P̂2 blocks with E8M0 scales)
   bool p_direct;    // direct-P ablation (Tab1b): P̂ = φ(P̃) relative to the running max, s_P1 = 1
+  bool p_qsum;      // NEXT #2 variant: l from the quantized P̂2 (tensor-core ones column, reading n2)
   int64_t unit_begin, unit_end;  // work units [begin, end) of the flattened (b·h, q-tile) space
 };
 

@@ -348,3 +348,54 @@ def test_direct_p_rejects_smoothing_q():
     qkv = s3.sage3_quantize_qkv(Q, K, V, smooth_q=True)
     with pytest.raises(s3.Sage3Error):
         s3.sage3_attn_fwd(qkv, p_quant="direct")
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("N,d", [(1, 64), (100, 128), (128, 64), (300, 128), (1024, 128), (2100, 64)])
+def test_qsum_variant_parity(N, d, causal):
+    """NEXT #2 row-sum variant (p_quant = "qsum", reading n2): l from the tensor core's ones-column product of the
+    quantized P̂2, against the oracle's PMODE_QSUM on the same codes (both gates of tests/parity.py), LSE, and the
+    unit-range form bitwise."""
+    B, H = 1, 2
+    Q, K, V = synth.make_qkv(B, H, N, d, seed=23 * N + d, dtype=torch.bfloat16, device="cuda")
+    qkv = s3.sage3_quantize_qkv(Q, K, V)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device="cuda")
+    O = s3.sage3_attn_fwd(qkv, causal=causal, out_dtype=torch.float32, lse=lse, p_quant="qsum")
+    torch.cuda.synchronize()
+    rows = np.arange(N, dtype=np.int32) if N <= 1024 else np.arange(0, N, 5, dtype=np.int32)
+    ref, ref_lse, amb, vmax = oracle_attention(oracle_heads(qkv, range(B * H)), causal=causal,
+                                               scale=1 / math.sqrt(d), p_mode=oracle.PMODE_QSUM, rows=rows)
+    for bh in range(B * H):
+        check(O[0, bh].cpu().numpy()[rows], ref[bh], torch.float32, f"head {bh}", amb=amb[bh], vmax=vmax[bh])
+    # LSE = scale·m + ln l with l from the quantized P: a P code decided the other way at a rounding midpoint (the
+    # decisions the element-wise bound allows for) moves l too, so a few rows may differ by up to a few 1e-3
+    dl = np.abs(lse.cpu().numpy().reshape(B * H, N)[:, rows] - ref_lse)
+    assert np.mean(dl > 1e-4 + 1e-5 * np.abs(ref_lse)) <= 0.01 and dl.max() <= 5e-3, (np.mean(dl > 1e-4), dl.max())
+    O2 = torch.zeros_like(O)
+    n = s3.n_units(qkv)
+    s3.sage3_attn_fwd_ex(qkv, O2, causal=causal, p_quant="qsum", unit_begin=0, unit_end=n // 2)
+    s3.sage3_attn_fwd_ex(qkv, O2, causal=causal, p_quant="qsum", unit_begin=n // 2)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O2)
+
+
+def test_qsum_constant_values_exact_on_gpu():
+    """The variant's defining property on the GPU: with every V row equal, O equals that row (the weights are
+    normalised by their own tensor-core sum) up to fp32 accumulation."""
+    N, d = 1000, 128
+    Q, K, V = synth.make_qkv(1, 1, N, d, seed=5, dtype=torch.bfloat16, device="cuda")
+    V = V[:, :, :1].expand(1, 1, N, d).contiguous()
+    qkv = s3.sage3_quantize_qkv(Q, K, V)
+    O = s3.sage3_attn_fwd(qkv, causal=True, out_dtype=torch.float32, p_quant="qsum")
+    torch.cuda.synchronize()
+    g = decode_head(qkv, 0)
+    cdeq = oracle.dequant_fmt(g["v_codes"], np.ascontiguousarray(g["v_sf_full"][:d]), 0)[:, 0]
+    np.testing.assert_allclose(O[0, 0].cpu().numpy(), np.broadcast_to(cdeq, (N, d)), rtol=2e-6, atol=1e-7)
+
+
+def test_qsum_rejects_mxfp4_and_smoothing_q():
+    Q, K, V = synth.make_qkv(1, 1, 256, 64, seed=2, dtype=torch.bfloat16, device="cuda")
+    for kw in ({"fmt": "mxfp4"}, {"smooth_q": True}):
+        qkv = s3.sage3_quantize_qkv(Q, K, V, **kw)
+        with pytest.raises(s3.Sage3Error):
+            s3.sage3_attn_fwd(qkv, p_quant="qsum")
