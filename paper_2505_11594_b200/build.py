@@ -20,7 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsage3.so")
 OBJ_CACHE = os.path.join(ROOT, "build", "obj")
-SOURCES = ["abi.cu", "quant.cu", "attn.cu", "attn_lazy.cu", "quant_i8.cu", "attn_i8.cu", "bwd_i8.cu"]
+SOURCES = ["abi.cu", "quant.cu", "attn.cu", "attn_lazy.cu", "attn_tmem.cu", "quant_i8.cu", "attn_i8.cu", "bwd_i8.cu"]
 HEADERS = ["sm100.cuh", "attn_common.cuh", "internal.h", os.path.join("..", "..", "include", "sage3.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC"]
@@ -39,22 +39,24 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    """Compile libsage3.so (or `out`, with extra -D `defines`, for experiments)."""
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=(), only=None) -> str:
+    """Compile libsage3.so (or `out`, with extra -D `defines`, for experiments; `only`: the sources the defines
+    apply to, the others built with the default flags)."""
     target = out or LIB
     if out is None and not force and not stale():
         return LIB
     os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
     tmpdir = tempfile.mkdtemp(prefix="sage3build")
     try:
-        common = [*NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
-                  "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+        base = [*NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+        flags = lambda src: base + ([f"-D{d}" for d in defines] if only is None or src in only else [])
 
         hdr = b"".join(open(os.path.join(CSRC, h), "rb").read() for h in HEADERS)
 
         def obj(src):
             # objects are cached by content (source, headers, flags) under build/obj: variant builds for A/B runs
             # only recompile the files their -D flags can change
+            common = flags(src)
             key = hashlib.sha1(open(os.path.join(CSRC, src), "rb").read() + hdr + " ".join(common).encode()).hexdigest()
             cached = os.path.join(OBJ_CACHE, f"{src[:-3]}-{key[:16]}.o")
             if not os.path.exists(cached):

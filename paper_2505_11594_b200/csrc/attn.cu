@@ -101,7 +101,7 @@ constexpr int kSBufs = 3;
 // otherwise unused columns 416..431 (tile j -> slot j % 8).  The softmax warp writes its rows' pair with
 // tcgen05.st before its p_full arrival; the correction reads it after pv_full (the PV MMA of the same tile was
 // issued after p_full), so the hand-off needs no mbarrier of its own.
-constexpr uint32_t kColX = 416;
+[[maybe_unused]] constexpr uint32_t kColX = 416;
 // Row-sum variant (kQSum, p_quant = SAGE3_P_TWO_LEVEL_QSUM, reading n2): l accumulates the quantized P,
 // computed by the tensor core as P̂2 (M=128, K=128) times a 16-column all-ones FP4 matrix (scales 1.0) into 16
 // TMEM columns per S/PV buffer (tile j -> kColRS + 16 (j % 3)); the ones operand's scale factors sit at kColSF1.
@@ -553,8 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       auto finish = [&](int c, const f2(&y)[16]) {
-        const float sA = c == 0 ? sdec[0] : c == 1 ? sdec[2] : c == 2 ? sdec[4] : sdec[6];
-        const float sB = c == 0 ? sdec[1] : c == 1 ? sdec[3] : c == 2 ? sdec[5] : sdec[7];
+        [[maybe_unused]] const float sA = c == 0 ? sdec[0] : c == 1 ? sdec[2] : c == 2 ? sdec[4] : sdec[6];
+        [[maybe_unused]] const float sB = c == 0 ? sdec[1] : c == 1 ? sdec[3] : c == 2 ? sdec[5] : sdec[7];
         uint32_t w[4];
 #pragma unroll
         for (int hb = 0; hb < 2; ++hb) {
@@ -788,8 +788,15 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
+#ifndef SAGE3_TMEM_O
+#define SAGE3_TMEM_O 0  // 1: the NVFP4 two-level / row-sum paths without smoothing Q run attn_tmem.cu's kernel
+#endif
+
 template <bool kMX>
 cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
+  if constexpr (!kMX) {
+    if (SAGE3_TMEM_O && !a.p_direct && !a.ds) return launch_attention_tmem(a, stream);
+  }
   if (a.p_direct) {  // ablation: no smoothing-Q instantiation (rejected in abi.cu)
     return a.d == 128 ? launch_d<128, false, kMX, true>(a, stream) : launch_d<64, false, kMX, true>(a, stream);
   }
