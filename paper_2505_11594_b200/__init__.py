@@ -128,8 +128,27 @@ def _stream(stream) -> ctypes.c_void_p:
 
 
 def _t4(x: torch.Tensor) -> Tensor4:
-    assert x.dim() == 4 and x.stride(3) == 1, "expected [B, H, N, d] with unit d-stride"
+    if x.dim() != 4 or x.stride(3) != 1:
+        raise Sage3Error(f"expected a [B, H, N, d] tensor with unit d-stride, got shape {tuple(x.shape)} "
+                         f"strides {tuple(x.stride())}")
     return Tensor4(x.data_ptr(), x.stride(0), x.stride(1), x.stride(2))
+
+
+def _check_out(o: torch.Tensor, shape, device, what: str):
+    """An output the kernels write with the problem's B, H, N, d: shape and device must match exactly (the C ABI
+    only sees a pointer and strides)."""
+    if tuple(o.shape) != tuple(shape):
+        raise Sage3Error(f"{what}: output shape {tuple(o.shape)} != {tuple(shape)}")
+    if o.device != device:
+        raise Sage3Error(f"{what}: output on {o.device}, inputs on {device}")
+
+
+def _check_lse(lse: torch.Tensor | None, n: int, device, what: str):
+    if lse is None:
+        return
+    if lse.dtype != torch.float32 or not lse.is_contiguous() or lse.numel() != n or lse.device != device:
+        raise Sage3Error(f"{what}: lse must be a contiguous float32 tensor of B*H*N = {n} elements on {device}, got "
+                         f"{lse.dtype} {tuple(lse.shape)} contiguous={lse.is_contiguous()} on {lse.device}")
 
 
 def version() -> str:
@@ -200,9 +219,13 @@ def sage3_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: F
     """Alg1 L2 + L7 (smoothing K, FP4 φ of Q, K, V; + L5 / L8's GEMV with smooth_q): see include/sage3.h.
     The format of a given `out` is its own (fmt applies when out is None)."""
     B, H, N, d = q.shape
-    assert k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dtype in (torch.float16, torch.bfloat16)
+    if not (k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype
+            and q.dtype in (torch.float16, torch.bfloat16) and q.device == k.device == v.device):
+        raise Sage3Error("sage3_quantize_qkv: q, k, v must share shape, device and a 16-bit float dtype")
     if out is None:
         out = FP4QKV(B, H, N, d, q.device, smooth_q=smooth_q, fmt=fmt)
+    elif (out.B, out.H, out.N, out.d) != (B, H, N, d) or out.q_data.device != q.device:
+        raise Sage3Error(f"sage3_quantize_qkv: out holds {(out.B, out.H, out.N, out.d)} on {out.q_data.device}")
     flag = ctypes.c_void_p(nonfinite.data_ptr() if nonfinite is not None else None)
     st = load().sage3_quantize_qkv(_t4(q), _t4(k), _t4(v), _DT[q.dtype], B, H, N, d, ctypes.byref(out.struct),
                                    ctypes.c_void_p(out.workspace.data_ptr()), out.workspace.numel(), flag,
@@ -218,6 +241,8 @@ def sage3_attn_fwd(qkv: FP4QKV, o: torch.Tensor | None = None, *, causal: bool =
     p_quant="direct" selects the Tab1b ablation (sage3_attn_fwd_ex)."""
     if o is None:
         o = torch.empty(qkv.B, qkv.H, qkv.N, qkv.d, dtype=out_dtype, device=qkv.q_data.device)
+    _check_out(o, (qkv.B, qkv.H, qkv.N, qkv.d), qkv.q_data.device, "sage3_attn_fwd")
+    _check_lse(lse, qkv.B * qkv.H * qkv.N, qkv.q_data.device, "sage3_attn_fwd")
     if p_quant != "two_level":
         return sage3_attn_fwd_ex(qkv, o, causal=causal, softmax_scale=softmax_scale, lse=lse, stream=stream,
                                  p_quant=p_quant)
@@ -234,6 +259,8 @@ def sage3_attn_fwd_ex(qkv: FP4QKV, o: torch.Tensor, *, causal: bool = False, sof
     """sage3_attn_fwd_ex: the attention with a sage3_attn_options struct (P quantization mode, unit range)."""
     if p_quant not in _PQ:
         raise Sage3Error(f"unknown p_quant {p_quant!r}")
+    _check_out(o, (qkv.B, qkv.H, qkv.N, qkv.d), qkv.q_data.device, "sage3_attn_fwd_ex")
+    _check_lse(lse, qkv.B * qkv.H * qkv.N, qkv.q_data.device, "sage3_attn_fwd_ex")
     opts = AttnOptions(1 if causal else 0, float(softmax_scale), _PQ[p_quant], 0, int(unit_begin), int(unit_end))
     lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
     st = load().sage3_attn_fwd_ex(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], ctypes.byref(opts), lse_p,
@@ -250,6 +277,8 @@ def n_units(qkv: FP4QKV) -> int:
 def sage3_attn_fwd_units(qkv: FP4QKV, o: torch.Tensor, unit_begin: int, unit_end: int, *, causal: bool = False,
                          softmax_scale: float = 0.0, lse: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """sage3_attn_fwd on the work units [unit_begin, unit_end) only (rows of o outside them untouched)."""
+    _check_out(o, (qkv.B, qkv.H, qkv.N, qkv.d), qkv.q_data.device, "sage3_attn_fwd_units")
+    _check_lse(lse, qkv.B * qkv.H * qkv.N, qkv.q_data.device, "sage3_attn_fwd_units")
     lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
     st = load().sage3_attn_fwd_units(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], 1 if causal else 0,
                                      float(softmax_scale), lse_p, int(unit_begin), int(unit_end), _stream(stream))
@@ -266,7 +295,10 @@ def sage3_forward_host(q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch
     """Host-buffer end-to-end path (H2D, quantize, attention, D2H enqueued on `stream`; not synchronized)."""
     B, H, N, d = q_host.shape
     for t in (q_host, k_host, v_host, o_host):
-        assert t.device.type == "cpu" and t.is_contiguous()
+        if t.device.type != "cpu" or not t.is_contiguous() or tuple(t.shape) != (B, H, N, d):
+            raise Sage3Error("sage3_forward_host: q, k, v, o must be contiguous host tensors of one [B, H, N, d] shape")
+    if not (q_host.dtype == k_host.dtype == v_host.dtype):
+        raise Sage3Error("sage3_forward_host: q, k, v must share a dtype")
     st = load().sage3_forward_host(ctypes.c_void_p(q_host.data_ptr()), ctypes.c_void_p(k_host.data_ptr()),
                                    ctypes.c_void_p(v_host.data_ptr()), _DT[q_host.dtype], B, H, N, d,
                                    1 if causal else 0, float(softmax_scale), ctypes.c_void_p(o_host.data_ptr()),
@@ -311,9 +343,13 @@ def sage3_int8_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o
                             nonfinite: torch.Tensor | None = None, stream=None) -> INT8QKV:
     """Alg2 L2 + L4: smooth-K and per-block INT8 ψ of Q, K, V (see include/sage3.h)."""
     B, H, N, d = q.shape
-    assert k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dtype in (torch.float16, torch.bfloat16)
+    if not (k.shape == q.shape == v.shape and q.dtype == k.dtype == v.dtype
+            and q.dtype in (torch.float16, torch.bfloat16) and q.device == k.device == v.device):
+        raise Sage3Error("sage3_int8_quantize_qkv: q, k, v must share shape, device and a 16-bit float dtype")
     if out is None:
         out = INT8QKV(B, H, N, d, q.device)
+    elif (out.B, out.H, out.N, out.d) != (B, H, N, d) or out.q.device != q.device:
+        raise Sage3Error(f"sage3_int8_quantize_qkv: out holds {(out.B, out.H, out.N, out.d)} on {out.q.device}")
     flag = ctypes.c_void_p(nonfinite.data_ptr() if nonfinite is not None else None)
     st = load().sage3_int8_quantize_qkv(_t4(q), _t4(k), _t4(v), _DT[q.dtype], B, H, N, d, ctypes.byref(out.struct),
                                         ctypes.c_void_p(out.workspace.data_ptr()), out.workspace.numel(), flag,
@@ -328,6 +364,8 @@ def sage3_int8_attn_fwd(qkv: INT8QKV, o: torch.Tensor | None = None, *, causal: 
     """Alg2 L6-L14 (INT8 QKᵀ, online softmax, per-token INT8 P, INT8 PV, O/l, lse)."""
     if o is None:
         o = torch.empty(qkv.B, qkv.H, qkv.N, qkv.d, dtype=out_dtype, device=qkv.q.device)
+    _check_out(o, (qkv.B, qkv.H, qkv.N, qkv.d), qkv.q.device, "sage3_int8_attn_fwd")
+    _check_lse(lse, qkv.B * qkv.H * qkv.N, qkv.q.device, "sage3_int8_attn_fwd")
     lse_p = ctypes.c_void_p(lse.data_ptr() if lse is not None else None)
     st = load().sage3_int8_attn_fwd(ctypes.byref(qkv.struct), _t4(o), _DT[o.dtype], 1 if causal else 0,
                                     float(softmax_scale), lse_p, _stream(stream))
@@ -349,10 +387,18 @@ def sage3_int8_attn_bwd(qkv: INT8QKV, v: torch.Tensor, o: torch.Tensor, dout: to
                         workspace: torch.Tensor | None = None, stream=None):
     """Alg3 (SageBwd backward): returns (dq, dk, dv) w.r.t. the unsmoothed q, k, v (see include/sage3.h)."""
     B, H, N, d = qkv.B, qkv.H, qkv.N, qkv.d
-    assert v.shape == dout.shape == o.shape == (B, H, N, d) and v.dtype == dout.dtype
-    assert lse.dtype == torch.float32 and lse.is_contiguous() and lse.numel() == B * H * N
+    dev = qkv.q.device
+    for t, nm in ((v, "v"), (dout, "dout"), (o, "o")):
+        _check_out(t, (B, H, N, d), dev, f"sage3_int8_attn_bwd {nm}")
+    if v.dtype != dout.dtype:
+        raise Sage3Error("sage3_int8_attn_bwd: v and dout must share a dtype")
+    if lse is None:
+        raise Sage3Error("sage3_int8_attn_bwd: lse is required")
+    _check_lse(lse, B * H * N, dev, "sage3_int8_attn_bwd")
     mk = lambda t: t if t is not None else torch.empty(B, H, N, d, dtype=grad_dtype, device=v.device)
     dq, dk, dv = mk(dq), mk(dk), mk(dv)
+    for t, nm in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        _check_out(t, (B, H, N, d), dev, f"sage3_int8_attn_bwd {nm}")
     if workspace is None:
         workspace = torch.empty(sage3_int8_bwd_workspace_bytes(B, H, N, d), dtype=torch.uint8, device=v.device)
     st = load().sage3_int8_attn_bwd(ctypes.byref(qkv.struct), _t4(v), _t4(o), _DT[o.dtype], _t4(dout), _DT[v.dtype],

@@ -37,6 +37,11 @@ bool tensor_ok(const sage3_tensor4& t, int esize) {
   if ((t.stride_n * esize) % 16 || (t.stride_h * esize) % 16 || (t.stride_b * esize) % 16) return false;
   return t.stride_n > 0 && t.stride_h >= 0 && t.stride_b >= 0;
 }
+// An OUTPUT the kernels write: additionally no zero head / batch stride where there is more than one head /
+// batch (several CTAs would write the same rows concurrently).
+bool out_tensor_ok(const sage3_tensor4& t, int esize, int B, int H) {
+  return tensor_ok(t, esize) && (H == 1 || t.stride_h != 0) && (B == 1 || t.stride_b != 0);
+}
 
 sage3_status device_ok() {
   int dev = 0, major = 0, minor = 0;
@@ -175,7 +180,7 @@ sage3_status sage3_attn_fwd_ex(const sage3_fp4_qkv* qkv, sage3_tensor4 o, sage3_
   if (unit_begin < 0 || unit_end < unit_begin || unit_end > n_units || unit_end - unit_begin > 0x7FFFFFFF)
     return SAGE3_ERR_INVALID_ARG;
   if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
-  if (!tensor_ok(o, esize_of(o_dtype))) return SAGE3_ERR_INVALID_ARG;
+  if (!out_tensor_ok(o, esize_of(o_dtype), qkv->B, qkv->H)) return SAGE3_ERR_INVALID_ARG;
   if (!qkv->q_data || !qkv->k_data || !qkv->v_data || !qkv->q_sf || !qkv->k_sf || !qkv->v_sf)
     return SAGE3_ERR_INVALID_ARG;
   if (!aligned16(qkv->q_data) || !aligned16(qkv->k_data) || !aligned16(qkv->v_data) || !aligned16(qkv->q_sf) ||
@@ -268,7 +273,7 @@ sage3_status sage3_int8_attn_fwd(const sage3_int8_qkv* qkv, sage3_tensor4 o, sag
   if (!qkv || !i8_shape_ok(qkv->B, qkv->H, qkv->N, qkv->d) || qkv->N_pad != npad(qkv->N))
     return SAGE3_ERR_INVALID_ARG;
   if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
-  if (!tensor_ok(o, esize_of(o_dtype))) return SAGE3_ERR_INVALID_ARG;
+  if (!out_tensor_ok(o, esize_of(o_dtype), qkv->B, qkv->H)) return SAGE3_ERR_INVALID_ARG;
   if (!qkv->q || !qkv->k || !qkv->v_t || !qkv->s_q || !qkv->s_k || !qkv->s_v) return SAGE3_ERR_INVALID_ARG;
   if (!aligned16(qkv->q) || !aligned16(qkv->k) || !aligned16(qkv->v_t)) return SAGE3_ERR_INVALID_ARG;
   if (!std::isfinite(softmax_scale)) return SAGE3_ERR_INVALID_ARG;
@@ -302,7 +307,9 @@ sage3_status sage3_int8_attn_bwd(const sage3_int8_qkv* qkv, sage3_tensor4 v, sag
   if (grad_dtype != SAGE3_FP16 && grad_dtype != SAGE3_BF16 && grad_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
   if (!tensor_ok(v, 2) || !tensor_ok(dout, 2) || !tensor_ok(o, esize_of(o_dtype))) return SAGE3_ERR_INVALID_ARG;
   const int ge = esize_of(grad_dtype);
-  if (!tensor_ok(dq, ge) || !tensor_ok(dk, ge) || !tensor_ok(dv, ge)) return SAGE3_ERR_INVALID_ARG;
+  if (!out_tensor_ok(dq, ge, qkv->B, qkv->H) || !out_tensor_ok(dk, ge, qkv->B, qkv->H) ||
+      !out_tensor_ok(dv, ge, qkv->B, qkv->H))
+    return SAGE3_ERR_INVALID_ARG;
   if (!qkv->q || !qkv->k || !qkv->s_q || !qkv->s_k || !qkv->k_mean || !lse) return SAGE3_ERR_INVALID_ARG;
   if (!aligned16(qkv->q) || !aligned16(qkv->k)) return SAGE3_ERR_INVALID_ARG;
   if (!std::isfinite(softmax_scale)) return SAGE3_ERR_INVALID_ARG;
@@ -355,6 +362,7 @@ sage3_status sage3_forward_host(const void* q_host, const void* k_host, const vo
   if (!q_host || !k_host || !v_host || !o_host || !scratch) return SAGE3_ERR_INVALID_ARG;
   if (!shape_ok(B, H, N, d)) return SAGE3_ERR_INVALID_ARG;
   if (in_dtype != SAGE3_FP16 && in_dtype != SAGE3_BF16) return SAGE3_ERR_UNSUPPORTED;
+  if (o_dtype != SAGE3_FP16 && o_dtype != SAGE3_BF16 && o_dtype != SAGE3_FP32) return SAGE3_ERR_UNSUPPORTED;
   const size_t need = sage3_forward_host_scratch_bytes(B, H, N, d, in_dtype, o_dtype);
   if (need == 0) return SAGE3_ERR_UNSUPPORTED;
   if (scratch_bytes < need) return SAGE3_ERR_WORKSPACE;
@@ -439,8 +447,22 @@ sage3_status sage3_forward_host(const void* q_host, const void* k_host, const vo
     ck(cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + h0 * head_out, dout + h0 * head_out, nh * head_out,
                        cudaMemcpyDeviceToHost, s_out));
   }
-  // join: the caller's stream waits for everything enqueued above (also on the error path, so that no
-  // library stream is left referencing caller memory unordered)
+  // join: the caller's stream waits for everything enqueued above on all three library streams (also on the
+  // error path, so that no library stream is left referencing caller memory unordered)
+  cudaStreamWaitEvent(s_out, start, 0);
+  {
+    cudaEvent_t c_done = nullptr, i_done = nullptr;
+    if (cudaEventCreateWithFlags(&c_done, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(c_done, s_cmp);
+      cudaStreamWaitEvent(s_out, c_done, 0);
+      cudaEventDestroy(c_done);
+    }
+    if (cudaEventCreateWithFlags(&i_done, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(i_done, s_in);
+      cudaStreamWaitEvent(s_out, i_done, 0);
+      cudaEventDestroy(i_done);
+    }
+  }
   ck(cudaEventRecord(out_done, s_out));
   cudaStreamWaitEvent(s_cmp, out_done, 0);
   cudaStreamWaitEvent(s, out_done, 0);

@@ -69,6 +69,17 @@ __device__ __forceinline__ void prod_wait(uint64_t* bar, uint32_t parity) {
   ptx::mbar_wait(bar, parity);
 #endif
 }
+// Which exp2 pairs of each 32-key chunk run on the FMA-pipe polynomial (bit i: pair i), per instantiation: the
+// share is 1/4 (two-level) or 5/16 (row-sum variant, whose softmax has no FADD2 row-sum tree); the positions were
+// picked by a same-box sweep of 12 masks (profiles/r2_poly_mask_sweep.txt; the spread is ±5% from ptxas scheduling).
+#ifndef SAGE3_POLY_MASK_TL
+#define SAGE3_POLY_MASK_TL 0x2222
+#endif
+#ifndef SAGE3_POLY_MASK_QS
+#define SAGE3_POLY_MASK_QS 0x1249
+#endif
+template <bool kQSum>
+constexpr uint32_t poly_mask() { return kQSum ? SAGE3_POLY_MASK_QS : SAGE3_POLY_MASK_TL; }
 constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
@@ -549,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float nbh = i < 8 ? nA : nB;
           const f2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2,
                              make_float2(nbh, nbh));
-          y[i] = ((kPolyMask >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          y[i] = ((poly_mask<kQSum>() >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
         }
       };
       auto finish = [&](int c, const f2(&y)[16]) {
@@ -757,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
 cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
   using L = Layout<D, kMX, kQSum>;
-  static bool attr_done[64] = {};
+  static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
@@ -788,15 +799,8 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
-#ifndef SAGE3_TMEM_O
-#define SAGE3_TMEM_O 0  // 1: the NVFP4 two-level / row-sum paths without smoothing Q run attn_tmem.cu's kernel
-#endif
-
 template <bool kMX>
 cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
-  if constexpr (!kMX) {
-    if (SAGE3_TMEM_O && !a.p_direct && !a.ds) return launch_attention_tmem(a, stream);
-  }
   if (a.p_direct) {  // ablation: no smoothing-Q instantiation (rejected in abi.cu)
     return a.d == 128 ? launch_d<128, false, kMX, true>(a, stream) : launch_d<64, false, kMX, true>(a, stream);
   }

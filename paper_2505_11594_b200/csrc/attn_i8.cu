@@ -6,8 +6,9 @@
 // by the per-block s_Q·s_K in the softmax; per-token P (Alg2 L10) in tile-local form
 //     P̂_ij = RNE(127 · 2^{sl2 (S − tmax_j)})  (= P̃/s_P with s_P = exp(scale(tmax_j − m_j))/127)
 //     O += MM(P̂_ij, V̂_j) · s_P · s_V_j  =  PV_int · 2^{sl2 (tmax_j − m)} / 127 · s_V_j
-// l from the unquantized P̃ (reading c9's analog, b5).  int32 -> fp32 conversions use the exact magic-number
-// trick (|S|, |PV| <= 127·127·128 < 2^22).
+// l from the unquantized P̃ (reading c9's analog, b5).  int32 -> fp32 conversions are I2F by default
+// (SAGE3_I8_I2F=1: exact, |S|, |PV| <= 127·127·128 < 2^24); the magic-number add (exact below 2^22) remains only
+// as the SAGE3_I8_I2F=0 alternative.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -437,7 +438,7 @@ bool make_map_i8(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t 
 template <int D>
 cudaError_t launch_i8_d(const I8AttnArgs& a, cudaStream_t stream) {
   using L = I8Layout<D>;
-  static bool attr_done[64] = {};
+  static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {

@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
 template <int D, bool kMX>
 cudaError_t launch_lazy_d(const AttnArgs& a, cudaStream_t stream) {
   using L = LazyLayout<D, kMX>;
-  static bool attr_done[64] = {};
+  static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {

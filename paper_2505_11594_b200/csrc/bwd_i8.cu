@@ -884,7 +884,7 @@ bool map_16(CUtensorMap* m, const void* base, int B, int H, int N, int D, int64_
 template <int D>
 cudaError_t launch_bwd_d(const I8BwdArgs& a, cudaStream_t stream) {
   using L = BLayout<D>;
-  static bool attr_done[64] = {};
+  static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 namespace sage3 {
@@ -98,7 +99,5 @@ struct AttnArgs {
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream);
 // The NEXT #2 lazy-reference variant (attn_lazy.cu; p_quant = SAGE3_P_TWO_LEVEL_LAZY, no smoothing Q).
 cudaError_t launch_attention_lazy(const AttnArgs& a, cudaStream_t stream);
-// The same two-level (or row-sum) numerics with O accumulated by the tensor core in TMEM (attn_tmem.cu).
-cudaError_t launch_attention_tmem(const AttnArgs& a, cudaStream_t stream);
 
 }  // namespace sage3

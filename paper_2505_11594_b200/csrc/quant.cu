@@ -470,7 +470,7 @@ bool make_input_map(CUtensorMap* m, const void* base, int B, int H, int N, int d
 template <typename T, int D, bool kMX>
 cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t stream) {
   using L = QL<D>;
-  static bool attr_done[64] = {};  // per instantiation
+  static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)  // per instantiation
   static int n_sm[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);

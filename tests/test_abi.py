@@ -110,3 +110,40 @@ def test_int8_bwd_host_checks(lib):
     assert args(ctypes.byref(q), t, None, s3.SAGE3_FP32, 1 << 20, 1 << 30) == s3.SAGE3_ERR_INVALID_ARG  # null lse
     assert args(ctypes.byref(q), t, 16, 7, 1 << 20, 1 << 30) == s3.SAGE3_ERR_UNSUPPORTED  # gradient dtype
     assert args(ctypes.byref(q), t, 16, s3.SAGE3_FP32, 1 << 20, 16) == s3.SAGE3_ERR_WORKSPACE
+
+
+class _FakeStream:  # the argument checks below return before anything is enqueued
+    cuda_stream = 0
+
+
+def test_binding_rejects_mismatched_outputs_before_the_call(lib):
+    """an output whose shape or device does not match the problem, or a wrong lse, is refused in the
+    binding (the C ABI only sees pointers and strides, and would write B*H*N rows)."""
+    import torch
+
+    qkv = s3.FP4QKV(1, 2, 200, 64, "cpu")
+    st = _FakeStream()
+    for bad in (torch.empty(1, 1, 200, 64), torch.empty(1, 2, 199, 64), torch.empty(2, 2, 200, 64)):
+        with pytest.raises(s3.Sage3Error):
+            s3.sage3_attn_fwd(qkv, bad, stream=st)
+        with pytest.raises(s3.Sage3Error):
+            s3.sage3_attn_fwd_units(qkv, bad, 0, 1, stream=st)
+    o = torch.empty(1, 2, 200, 64, dtype=torch.bfloat16)
+    for lse in (torch.empty(1, 2, 199), torch.empty(1, 2, 200, dtype=torch.float16), torch.empty(2, 400)[:, ::2]):
+        with pytest.raises(s3.Sage3Error):
+            s3.sage3_attn_fwd(qkv, o, lse=lse, stream=st)
+    with pytest.raises(s3.Sage3Error):
+        s3.sage3_forward_host(torch.empty(1, 2, 8, 64), torch.empty(1, 2, 8, 64), torch.empty(1, 2, 9, 64),
+                              torch.empty(1, 2, 8, 64), torch.empty(16, dtype=torch.uint8), stream=st)
+
+
+def test_abi_rejects_zero_head_stride_outputs(lib):
+    """with H > 1 (or B > 1) an output with a zero head (batch) stride would make CTAs write the same
+    rows concurrently; the ABI refuses it before any launch (no GPU needed to get the status)."""
+    import torch
+
+    qkv = s3.FP4QKV(1, 2, 200, 64, "cpu")
+    st = _FakeStream()
+    o = torch.empty(1, 1, 200, 64, dtype=torch.bfloat16).expand(1, 2, 200, 64)  # stride_h == 0
+    with pytest.raises(s3.Sage3Error, match="INVALID_ARG"):
+        s3.sage3_attn_fwd(qkv, o, stream=st)
