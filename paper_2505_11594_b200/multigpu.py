@@ -161,3 +161,114 @@ def _unpack(out: torch.Tensor, packed: torch.Tensor, u0: int, u1: int, T: int, N
     d = out.shape[-1]
     idx, valid = _row_index(u0, u1, T, N, 0, out.device)
     out.view(-1, d)[idx[valid]] = packed[: u1 - u0].reshape(-1, d)[valid]
+
+
+# ------------------------------------------------------------------------------------------------ launcher
+def self_launch(nprocs: int, argv: list[str], script: str) -> None:
+    """One process per GPU: when `nprocs` > 1 and this process was not started by torch.distributed.run (no
+    WORLD_SIZE in the environment), re-execute `script argv` under torch.distributed.run with nprocs ranks on
+    127.0.0.1 (this call then does not return).  Otherwise a no-op."""
+    import os
+    import socket
+    import sys
+
+    if nprocs <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nprocs}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), script, *argv]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def init_from_env(backend: str):
+    """(rank, world, local_rank) of a torchrun-launched process; initialises the default process group when
+    world > 1 (NCCL on GPUs, gloo for the CPU tests)."""
+    import os
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        kw = {}
+        if backend == "nccl":
+            kw["device_id"] = torch.device("cuda", local)
+        dist.init_process_group(backend, **kw)
+    return rank, world, local
+
+
+class ShardPlan:
+    """This rank's share of a B x H x N (x d) problem: its contiguous unit range [u0, u1) of the flattened
+    (b·h, query-tile) space (shard_units) and the heads [h0, h1) those units touch."""
+
+    def __init__(self, B: int, H: int, N: int, causal: bool, world: int, rank: int):
+        self.B, self.H, self.N, self.causal, self.world, self.rank = B, H, N, causal, world, rank
+        self.T = tiles_per_head(N)
+        self.ranges = shard_units(B, H, N, causal, world)
+        self.u0, self.u1 = self.ranges[rank]
+        self.h0 = self.u0 // self.T
+        self.h1 = (self.u1 - 1) // self.T + 1 if self.u1 > self.u0 else self.h0
+
+    def head_chunks(self, min_units: int = 0):
+        """(first head, head count, unit range numbered within those heads) of this rank's work, in order: the
+        pieces the pipelined gather sends as soon as each is computed.  Consecutive heads are merged until a piece
+        has at least `min_units` units (each piece is one quantize + one attention launch; a launch of a few
+        hundred 128-row tiles leaves the 148 SMs a partial last wave)."""
+        h = self.h0
+        while h < self.h1:
+            e = h + 1
+            while e < self.h1 and (min(self.u1, e * self.T) - max(self.u0, h * self.T)) < min_units:
+                e += 1
+            lo, hi = max(self.u0, h * self.T), min(self.u1, e * self.T)
+            yield h, e - h, lo - h * self.T, hi - h * self.T
+            h = e
+
+
+def pipelined_forward_gather(plan: ShardPlan, d: int, head_inputs, compute, *, dtype=None, device=None,
+                             gather_to: int = 0, group=None, min_units: int = 1024):
+    """Strong-scaling form of the launcher: this rank computes its units head by head and, for every finished
+    head, starts the transfer of that head's rows to rank `gather_to` (non-blocking point-to-point sends, so the
+    NCCL transfer of head h overlaps the compute of head h+1); rank `gather_to` posts all receives up front and
+    assembles O.  Returns O [B, H, N, d] on `gather_to` (None elsewhere).
+
+    head_inputs(h0, n) -> (q, k, v) [1, n, N, d] of flattened heads h0 .. h0+n-1 (each rank generates or loads only
+    its own); pieces of at least `min_units` units (one piece for the whole range when there is nothing to send);
+    compute(q, k, v, causal, scale, unit_lo, unit_hi) -> O [1, 1, N, d] valid on those units' rows (the CUDA path
+    by default: _default_compute)."""
+    rank, world, N, T = plan.rank, plan.world, plan.N, plan.T
+    fn = compute or _default_compute
+    out = None
+    recvs = []
+    if rank == gather_to:
+        out = torch.empty(plan.B * plan.H, N, d, dtype=dtype, device=device)
+        if world > 1:
+            for src in range(world):
+                if src == gather_to:
+                    continue
+                sp = ShardPlan(plan.B, plan.H, N, plan.causal, world, src)
+                for h, _, lo, hi in sp.head_chunks(min_units):
+                    buf = torch.empty((hi - lo) * TILE, d, dtype=dtype, device=device)
+                    recvs.append((dist.irecv(buf, src=src, group=group), buf, h, lo, hi))
+    sends = []
+    mu = min_units if world > 1 else plan.u1 - plan.u0  # nothing to overlap on one GPU: one piece
+    for h, nh, lo, hi in plan.head_chunks(mu):
+        q, k, v = head_inputs(h, nh)
+        o = fn(q, k, v, plan.causal, 0.0, lo, hi)[0]  # [nh, N, d]
+        idx, valid = _row_index(h * T + lo, h * T + hi, T, N, h, o.device)
+        rows = o.new_zeros((hi - lo) * TILE, d)
+        rows[valid] = o.reshape(-1, d)[idx[valid]]
+        if rank == gather_to:
+            _unpack(out, rows.view(-1, TILE, d), h * T + lo, h * T + hi, T, N)
+        else:
+            sends.append((dist.isend(rows, dst=gather_to, group=group), rows))
+    for w, _ in sends:
+        w.wait()
+    for w, buf, h, lo, hi in recvs:
+        w.wait()
+        _unpack(out, buf.view(-1, TILE, d), h * T + lo, h * T + hi, T, N)
+    if out is not None:
+        return out.view(plan.B, plan.H, N, d)
+    return None

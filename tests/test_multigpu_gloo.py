@@ -91,3 +91,39 @@ def test_forward_sharded_gather_world2(B, H, N, causal):
     assert ret["ok"] and ret["shape"] == (B, H, N, 8)
     s, e = shard_units(B, H, N, causal, 2)[1]
     assert ret["local1"][0] == e - s
+
+
+@pytest.mark.parametrize("nprocs,shape,causal,mu", [(2, "1,5,300,16", False, 0), (3, "2,3,700,8", True, 7),
+                                                    (2, "1,1,128,8", True, 0)])
+def test_self_launch_pipelined_gather_gloo(nprocs, shape, causal, mu):
+    """The launcher end to end on CPU: self_launch re-executes under torch.distributed.run (127.0.0.1, gloo),
+    every rank computes its ShardPlan units head by head (host stub for the kernel) and sends each finished
+    head's rows to rank 0 (isend/irecv pipelined gather), which reassembles O exactly."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, os.path.join(root, "tools", "mg_selftest.py"), "--nprocs", str(nprocs), "--stub",
+           "--shape", shape, "--min-units", str(mu)] + (["--causal"] if causal else [])
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=dict(os.environ, OMP_NUM_THREADS="1"))
+    line = [x for x in p.stdout.splitlines() if x.startswith("MG_SELFTEST")]
+    assert line and line[0].startswith(f"MG_SELFTEST OK world={nprocs}"), p.stdout[-2000:] + p.stderr[-2000:]
+
+
+def test_shard_plan_head_chunks():
+    from paper_2505_11594_b200.multigpu import ShardPlan
+
+    # C4 strong scaling: 24 heads over 8 GPUs -> 3 whole heads per rank
+    p = ShardPlan(1, 24, 118800, False, 8, 3)
+    assert (p.h0, p.h1) == (9, 12) and [c[0] for c in p.head_chunks()] == [9, 10, 11]
+    assert all(n == 1 and lo == 0 and hi == 929 for _, n, lo, hi in p.head_chunks())
+    assert list(p.head_chunks(1500)) == [(9, 2, 0, 1858), (11, 1, 0, 929)]
+    # C3 on 8 GPUs: a rank's range can start and end inside heads
+    T = tiles_per_head(17776)
+    for r in range(8):
+        p = ShardPlan(2, 30, 17776, False, 8, r)
+        for mu in (0, 200, 10 ** 9):
+            ch = list(p.head_chunks(mu))
+            assert sum(hi - lo for _, _, lo, hi in ch) == p.u1 - p.u0
+            assert all(0 <= lo < hi <= n * T for _, n, lo, hi in ch)
+            assert ch[0][0] == p.h0 and sum(n for _, n, _, _ in ch) == p.h1 - p.h0
