@@ -114,7 +114,7 @@ sage3_status sage3_smooth_q_sizes(int B, int H, int N, int d, size_t bytes[2]) {
 
 size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d) {
   if (!shape_ok(B, H, N, d)) return 0;
-  return (size_t)B * H * (size_t)(npad(N) / 128) * d * sizeof(double);
+  return sage3::quant_sums_bytes(B * H, (int)(npad(N) / 128), d) + sage3::quant_ctl_bytes(B * H);
 }
 
 int sage3_kv_tile(int d) { return (d == 64 || d == 128) ? 128 : 0; }

@@ -8,6 +8,11 @@
 
 namespace sage3 {
 
+// Quantize workspace: the fp64 K chunk sums [BH][d][Np/128], then the fused K-mean control words (a work counter and
+// per head {chunk sums added, km ready}), zeroed by the launcher before each call.
+inline size_t quant_sums_bytes(int BH, int nch, int d) { return ((size_t)BH * nch * d * 8 + 255) & ~size_t(255); }
+inline size_t quant_ctl_bytes(int BH) { return ((size_t)16 + (size_t)BH * 8 + 255) & ~size_t(255); }
+
 struct QKArgs {
   const void* q;
   const void* k;

@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include <cudaTypedefs.h>
@@ -155,6 +156,69 @@ __global__ void __launch_bounds__(256) kmean_final_kernel(const double* __restri
 //         per channel; scale bytes of every item go to its SF atoms staged in smem, then 16-byte stores.
 constexpr int kQStages = 3;
 
+// The fused K-mean path below is selected at run time with the environment variable SAGE3_QUANT_FUSED_K=1 (off by
+// default).  Measured on the B200 (B=1, H=32, N=32K): it moves 1.00 GB of DRAM per call instead of
+// 1.29 GB (K is read once), but takes 280-336 µs against 269 µs for the three-launch path: the per-head dependency
+// (all chunk sums, then km, then φ(K − km)) and the sequential fp64 reductions of reading c10 cost more latency
+// than the 0.26 GB of re-read saves.
+// Fused K mean (reading c10 unchanged): K is read from HBM once.  Work items are handed out in this global order
+// by an atomic counter (an item only depends on items with smaller indices, every claimed item sits on a resident
+// CTA that processes its items in increasing order, so waiting cannot deadlock):
+//   KS_0, F_0, KS_1, F_1, KS_2, KQ_0, F_2, KS_3, KQ_1, F_3, ..., KQ_{G-2}, KQ_{G-1}   (KQ_g after KS_{g+2})
+// KS_g: the fp64 chunk sums of the K tiles of head group g (HBM read, kept in L2: evict_last hint); KQ_g: φ(K − km)
+// of the same tiles (L2 hits) once the group's heads have their km; F_g: an equal share of the Q and Vᵀ items
+// (evict_first), the distance that lets every KS_g item finish (≈ CTAs x ring depth items are in flight) before
+// KQ_g is claimed.  A group holds kKGroupBytes of K, so the groups in flight stay well inside the 126 MB L2.  The
+// CTA that adds a head's last chunk sum reduces the head's chunk sums in ascending order (the c10 order), writes
+// km and releases a per-head flag the KQ items acquire.
+#ifndef SAGE3_KGROUP_MB
+#define SAGE3_KGROUP_MB 8
+#endif
+constexpr int64_t kKGroupBytes = (int64_t)SAGE3_KGROUP_MB << 20;
+enum : int { kItemQ = 0, kItemV = 1, kItemKQ = 2, kItemKS = 3 };
+struct ItemPlan {
+  static constexpr int kLag = 2;  // KQ_g is claimed after KS_{g+kLag}: two groups + fillers of distance
+  int BH, nch, GK, G, F;  // heads, chunks per head, heads per K group, groups, filler (Q/Vᵀ) items per group
+  __host__ __device__ int group_heads(int g) const { return min(GK, BH - g * GK); }
+  __host__ __device__ int total() const { return 4 * BH * nch; }  // KS, KQ, Q, Vᵀ
+  __host__ __device__ int filler(int g) const { return max(0, min(F, 2 * BH * nch - g * F)); }
+  // item index -> (kind, flattened head, chunk)
+  __device__ void decode(int idx, int& kind, int& bh, int& chunk) const {
+    auto in_group = [&](int k, int g, int off) { kind = k, bh = g * GK + off / nch, chunk = off % nch; };
+    auto in_filler = [&](int g, int off) {
+      const int f = g * F + off, per = BH * nch;  // Q items, then Vᵀ items
+      kind = f < per ? kItemQ : kItemV;
+      const int r = f < per ? f : f - per;
+      bh = r / nch, chunk = r % nch;
+    };
+    for (int g = 0; g < G + kLag; ++g) {
+      if (g < G) {
+        const int sg = group_heads(g) * nch;
+        if (idx < sg) return in_group(kItemKS, g, idx);
+        idx -= sg;
+      }
+      if (g >= kLag) {
+        const int sq = group_heads(g - kLag) * nch;
+        if (idx < sq) return in_group(kItemKQ, g - kLag, idx);
+        idx -= sq;
+      }
+      if (g < G) {
+        const int fg = filler(g);
+        if (idx < fg) return in_filler(g, idx);
+        idx -= fg;
+      }
+    }
+    kind = -1;  // (unreachable for idx < total())
+  }
+};
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// per-call control words in the quantize workspace (after the chunk sums), zeroed by the launcher
+struct QCtl {
+  uint32_t next;    // work counter
+  uint32_t pad[3];
+  // then BH x {chunk-sum count, km ready}
+};
+
 template <int D>
 struct QL {
   static constexpr int kTile = 128 * D * 2;
@@ -168,11 +232,12 @@ struct QL {
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-template <typename T, int D, bool kMX>
+template <typename T, int D, bool kMX, bool kFusedK>
 __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                               const __grid_constant__ CUtensorMap tm_k,
                                                               const __grid_constant__ CUtensorMap tm_v, QKArgs qa,
-                                                              VArgs va) {
+                                                              VArgs va, ItemPlan ip, double* __restrict__ ws,
+                                                              uint32_t* __restrict__ ctl) {
   using L = QL<D>;
   extern __shared__ uint8_t qsm_raw[];
   __shared__ float s_rcp[128];  // fl32(1/s) per E4M3 scale code (c4); 0 for s = 0
@@ -180,9 +245,12 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(qsm_raw) + 127) & ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::oBar);
   uint64_t* empty = full + kQStages;
+  __shared__ int4 s_item[kQStages];  // kFusedK: (kind, head, chunk) of each ring stage (kind -1: no more work)
+  __shared__ int s_last;            // kFusedK: this CTA added a head's last chunk sum
   const int t = threadIdx.x, warp = t >> 5;
   const int nch = qa.Np >> 7, BH = qa.B * qa.H;
   const int per_tensor = BH * nch, total = 3 * per_tensor;
+  uint32_t* head_cnt = ctl + 4;  // [BH][2]: chunk sums added, km ready
   if (t == 0) {
     for (int s = 0; s < kQStages; ++s) {
       mbar_init(&full[s], 1);
@@ -199,6 +267,34 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
   __syncthreads();
 
   if (warp == 8) {  // ---------------------------------------------------------------- TMA producer
+    if constexpr (kFusedK) {
+      if (elect_one()) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+        const uint64_t keep = l2_policy_evict_last(), stream_once = l2_policy_evict_first();
+        int next = (int)atomicAdd(&ctl[0], 1u);  // the next item is claimed one stage ahead (atomic latency hidden)
+        for (int k = 0;; ++k) {
+          const int s = k % kQStages;
+          mbar_wait(&empty[s], ((uint32_t)(k / kQStages) & 1u) ^ 1u);
+          const int idx = next;
+          if (idx >= ip.total()) {
+            s_item[s] = make_int4(-1, 0, 0, 0);
+            mbar_arrive(&full[s]);  // completes the phase without a transfer
+            break;
+          }
+          next = (int)atomicAdd(&ctl[0], 1u);
+          int kind, bh, chunk;
+          ip.decode(idx, kind, bh, chunk);
+          s_item[s] = make_int4(kind, bh, chunk, 0);
+          const CUtensorMap* tm = kind == kItemQ ? &tm_q : kind == kItemV ? &tm_v : &tm_k;
+          mbar_arrive_expect_tx(&full[s], L::kTile);
+          tma_load_4d_hint(sm + s * L::kTile, tm, &full[s], 0, chunk * 128, bh % qa.H, bh / qa.H,
+                           kind == kItemKS ? keep : stream_once);
+        }
+      }
+      return;
+    }
     if (elect_one()) {
       prefetch_tmap(&tm_q);
       prefetch_tmap(&tm_k);
@@ -218,11 +314,70 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
   // ------------------------------------------------------------------------------------ consumers (256)
   bool finite = true;
   int k = 0;
-  for (int item = blockIdx.x; item < total; item += gridDim.x, ++k) {
+  for (int item = kFusedK ? 0 : blockIdx.x; kFusedK || item < total; item += gridDim.x, ++k) {
     const int s = k % kQStages;
-    const int tensor = item / per_tensor, rem = item % per_tensor, bh = rem / nch, chunk = rem % nch;
+    int tensor, bh, chunk;
     const T* tile = reinterpret_cast<const T*>(sm + s * L::kTile);
     mbar_wait(&full[s], (uint32_t)(k / kQStages) & 1u);
+    if constexpr (kFusedK) {
+      const int4 it = s_item[s];
+      if (it.x < 0) break;
+      const int kind = it.x;
+      bh = it.y, chunk = it.z;
+      if (kind == kItemKS) {
+        // chunk sums of K (reading c10): thread c sums channel c over the chunk's real tokens in ascending order
+        // in fp64 (rows >= N arrived as zeros); ws[bh][c][chunk]
+        if (t < D) {
+          double acc = 0.0;
+          const int nr = min(128, qa.N - chunk * 128);
+          for (int r = 0; r < nr; ++r) acc += (double)to_f32<T>(tile[r * D + t]);
+          ws[((int64_t)bh * nch + chunk) * D + t] = acc;  // [bh][chunk][channel]: the km pass reads rows
+        }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&empty[s]);
+        consumer_bar();  // the CTA's sums are written (CTA scope); thread 0's fence publishes them at gpu scope
+        if (t == 0) {
+          fence_acq_rel_gpu();
+          const bool last = atomicAdd(&head_cnt[2 * bh], 1u) == (uint32_t)nch - 1;
+          if (last) fence_acq_rel_gpu();  // acquire the other CTAs' sums of this head
+          s_last = last ? 1 : 0;
+        }
+        consumer_bar();
+        if (s_last) {  // this CTA completed the head: km = fl32(Σ_chunks / N), chunks in ascending order
+          if (t < D) {  // channel t: its chunk sums are a column of [chunk][channel] (coalesced rows), 16 in flight
+            const double* p = ws + (int64_t)bh * nch * D + t;
+            double tot = 0.0;
+            int c = 0;
+            for (; c + 16 <= nch; c += 16) {
+              double v[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = __ldcg(p + (int64_t)(c + i) * D);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) tot += v[i];
+            }
+            for (; c < nch; ++c) tot += __ldcg(p + (int64_t)c * D);
+            qa.k_mean[(int64_t)bh * D + t] = (float)(tot / (double)qa.N);
+          }
+          consumer_bar();
+          if (t == 0) {
+            fence_acq_rel_gpu();
+            atomicExch(&head_cnt[2 * bh + 1], 1u);
+          }
+        }
+        continue;
+      }
+      tensor = kind == kItemQ ? 0 : kind == kItemV ? 1 : 2;
+      if (tensor == 2) {  // φ(K − km) needs the head's km: wait for its release (all producing CTAs are resident)
+        if (t == 0) {
+          while (ld_acquire_u32(&head_cnt[2 * bh + 1]) == 0u) __nanosleep(64);
+        }
+        consumer_bar();
+      }
+    } else {
+      tensor = item / per_tensor;
+      const int rem = item % per_tensor;
+      bh = rem / nch, chunk = rem % nch;
+    }
     if (tensor != 1) {  // Q or K: φ along d
       const bool smooth = tensor == 2;
       const bool sub = smooth || qa.q_mean != nullptr;  // x = fl32(X - mean): K - km, or Q - q̄ (Alg1 L5)
@@ -245,8 +400,8 @@ __global__ void __launch_bounds__(288, 2) quant_stream_kernel(const __grid_const
       float km[8];
       if (sub) {
         const float* msrc = smooth ? qa.k_mean + (int64_t)bh * D + cv * 8 : s_qm + cv * 8;
-        const float4 m0 = reinterpret_cast<const float4*>(msrc)[0];
-        const float4 m1 = reinterpret_cast<const float4*>(msrc)[1];
+        const float4 m0 = smooth ? __ldcg(reinterpret_cast<const float4*>(msrc)) : reinterpret_cast<const float4*>(msrc)[0];
+        const float4 m1 = smooth ? __ldcg(reinterpret_cast<const float4*>(msrc) + 1) : reinterpret_cast<const float4*>(msrc)[1];
         km[0] = m0.x, km[1] = m0.y, km[2] = m0.z, km[3] = m0.w, km[4] = m1.x, km[5] = m1.y, km[6] = m1.z, km[7] = m1.w;
       }
       uint8_t* sfs = sm + L::oSFqk;
@@ -475,8 +630,11 @@ cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t 
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(quant_stream_kernel<T, D, kMX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         L::kAlloc);
+    cudaError_t e = cudaFuncSetAttribute(quant_stream_kernel<T, D, kMX, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(quant_stream_kernel<T, D, kMX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               L::kAlloc);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
     attr_done[dev] = true;
@@ -486,14 +644,33 @@ cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t 
       !make_input_map(&tk, qk.k, qk.B, qk.H, qk.N, D, qk.k_sb, qk.k_sh, qk.k_sn) ||
       !make_input_map(&tv, v.v, qk.B, qk.H, qk.N, D, v.sb, v.sh, v.sn))
     return cudaErrorInvalidValue;
-  const int BH = qk.B * qk.H;
-  dim3 grid(qk.Np / 128, BH);
-  kmean_kernel<T><<<grid, D / 2, 0, stream>>>(reinterpret_cast<const T*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn, qk.H,
-                                              qk.N, D, ws);
-  kmean_final_kernel<<<(BH * D * 32 + 255) / 256, 256, 0, stream>>>(ws, qk.Np / 128, qk.N, BH * D, qk.k_mean);
-  const int items = 3 * BH * (qk.Np / 128);
+  const int BH = qk.B * qk.H, nch = qk.Np / 128;
+  dim3 grid(nch, BH);
+  ItemPlan ip{};
+  ip.BH = BH, ip.nch = nch;
+  {
+    const int64_t gk = kKGroupBytes / ((int64_t)qk.Np * D * 2);
+    ip.GK = (int)(gk < 1 ? 1 : gk > BH ? BH : gk);
+  }
+  ip.G = (BH + ip.GK - 1) / ip.GK;
+  ip.F = (2 * BH * nch + ip.G - 1) / ip.G;
+  uint32_t* ctl = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(ws) + quant_sums_bytes(BH, nch, D));
+  const int items = 3 * BH * nch;
   const int ctas = min(items, 2 * (dev < 64 && n_sm[dev] ? n_sm[dev] : 148));
-  quant_stream_kernel<T, D, kMX><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v);
+  static const bool fused_k = [] {
+    const char* e = std::getenv("SAGE3_QUANT_FUSED_K");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (fused_k) {
+    cudaError_t e = cudaMemsetAsync(ctl, 0, quant_ctl_bytes(BH), stream);
+    if (e != cudaSuccess) return e;
+    quant_stream_kernel<T, D, kMX, true><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v, ip, ws, ctl);
+  } else {
+    kmean_kernel<T><<<grid, D / 2, 0, stream>>>(reinterpret_cast<const T*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn, qk.H,
+                                                qk.N, D, ws);
+    kmean_final_kernel<<<(BH * D * 32 + 255) / 256, 256, 0, stream>>>(ws, nch, qk.N, BH * D, qk.k_mean);
+    quant_stream_kernel<T, D, kMX, false><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v, ip, ws, ctl);
+  }
   if (qk.q_mean) {  // smoothing Q: the GEMV term, after every q̄ of the head is written
     static bool ds_attr[64] = {};
     constexpr int kDsSmem = (D * 128 + D * 64) * 4;

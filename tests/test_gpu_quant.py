@@ -116,3 +116,18 @@ def test_quantize_smooth_q_bit_exact(d, N):
         bound = np.abs(want.q_mean).astype(np.float64) @ np.abs(want.ks).astype(np.float64).T
         err = np.abs(got["ds"][:, :N] - ref[:, :N])
         assert np.all(err <= 1e-6 * bound[:, :N] + 1e-30), err.max()
+
+
+def test_fused_k_mean_path_bit_exact():
+    """The optional fused K-mean quantizer (SAGE3_QUANT_FUSED_K=1: K read from HBM once, per-head chunk sums -> km ->
+    φ(K − km) in one persistent launch) gives the same bits: this file's bit-exact cases rerun under it."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_quant.py"),
+                        "-k", "(bit_exact and not fused) or strided or large_offset"],
+                       env=dict(os.environ, SAGE3_QUANT_FUSED_K="1"), capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+    assert " passed" in p.stdout
