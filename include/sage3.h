@@ -103,7 +103,8 @@ sage3_status sage3_fp4_qkv_sizes_fmt(int B, int H, int N, int d, int fmt, size_t
 /* Host-only size queries for smoothing Q: bytes[0] = q_mean, bytes[1] = ds (see sage3_fp4_qkv). */
 sage3_status sage3_smooth_q_sizes(int B, int H, int N, int d, size_t bytes[2]);
 
-/* Device workspace of sage3_quantize_qkv: fp64 K-mean partial sums, B*H*(N_pad/128)*d*8 bytes. */
+/* Device workspace of sage3_quantize_qkv: the fp64 K-mean chunk sums (B*H*(N_pad/128)*d*8 bytes, rounded up to 256)
+ * followed by the fused K-mean path's control words (16 + 8*B*H bytes, rounded up to 256). */
 size_t sage3_quantize_workspace_bytes(int B, int H, int N, int d);
 
 /* B_kv (keys per tile) used by sage3_attn_fwd for head dim d.  The per-tile first-level P scale s_P1

@@ -45,7 +45,9 @@ def test_size_queries(lib):
     Np = 384
     sizes = s3.sage3_fp4_qkv_sizes(B, H, N, d)
     assert sizes == [B * H * Np * d // 2] * 3 + [B * H * Np * d // 16] * 2 + [B * H * 128 * Np // 16, B * H * d * 4]
-    assert s3.sage3_quantize_workspace_bytes(B, H, N, d) == B * H * (Np // 128) * d * 8
+    # fp64 chunk sums [BH][d][Np/128] (256-byte aligned) + the fused K-mean control words (16 + 8 per head, aligned)
+    al = lambda x: (x + 255) // 256 * 256
+    assert s3.sage3_quantize_workspace_bytes(B, H, N, d) == al(B * H * (Np // 128) * d * 8) + al(16 + 8 * B * H)
     with pytest.raises(s3.Sage3Error):
         s3.sage3_fp4_qkv_sizes(1, 1, 0, 64)
     with pytest.raises(s3.Sage3Error):
