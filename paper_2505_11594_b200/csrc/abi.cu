@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "../../include/sage3.h"
 #include "internal.h"
@@ -27,6 +28,58 @@ bool shape_ok(int B, int H, int N, int d) {
   return true;
 }
 
+}  // namespace
+
+namespace sage3 {
+CUresult encode_tiled_cached(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, CUtensorMapDataType dt,
+                             cuuint32_t rank, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                             const cuuint32_t* box, const cuuint32_t* es, CUtensorMapInterleave il,
+                             CUtensorMapSwizzle swz, CUtensorMapL2promotion promo, CUtensorMapFloatOOBfill oob) {
+  // key: every argument, as bytes (rank <= 5)
+  struct Key {
+    uint64_t w[24];
+    bool operator==(const Key& o) const { return std::memcmp(w, o.w, sizeof(w)) == 0; }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      uint64_t h = 1469598103934665603ull;
+      for (uint64_t x : k.w) h = (h ^ x) * 1099511628211ull;
+      return (size_t)h;
+    }
+  };
+  Key k{};
+  k.w[0] = (uint64_t)dt | ((uint64_t)rank << 8) | ((uint64_t)il << 16) | ((uint64_t)swz << 24) |
+           ((uint64_t)promo << 32) | ((uint64_t)oob << 40);
+  k.w[1] = reinterpret_cast<uint64_t>(base);
+  for (cuuint32_t i = 0; i < rank && i < 5; ++i) {
+    k.w[2 + i] = dims[i];
+    k.w[7 + i] = i + 1 < rank ? strides[i] : 0;
+    k.w[12 + i] = ((uint64_t)box[i] << 32) | es[i];
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k.w[17] = (uint64_t)dev;
+  static std::mutex mu;
+  static std::unordered_map<Key, CUtensorMap, Hash> cache;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(k);
+    if (it != cache.end()) {
+      *m = it->second;
+      return CUDA_SUCCESS;
+    }
+  }
+  const CUresult r = enc(m, dt, rank, base, dims, strides, box, es, il, swz, promo, oob);
+  if (r == CUDA_SUCCESS) {
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() >= 1024) cache.clear();  // bounded: buffers of a long-running process come and go
+    cache.emplace(k, *m);
+  }
+  return r;
+}
+}  // namespace sage3
+
+namespace {
 int64_t npad(int N) { return ((int64_t)N + 127) / 128 * 128; }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include "internal.h"
 #include "sm100.cuh"
 
 namespace sage3 {
@@ -268,7 +269,7 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t row
   cuuint32_t box[2] = {box_bytes, box_rows};
   cuuint32_t es[2] = {1, 1};
   const CUtensorMapSwizzle swz = box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+  return encode_tiled_cached(enc, m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -286,7 +287,7 @@ bool make_map_o(CUtensorMap* m, const void* base, int dt, int B, int H, int N, i
   cuuint64_t strides[3] = {(cuuint64_t)sn * es, (cuuint64_t)sh * es, (cuuint64_t)sb * es};
   cuuint32_t box[4] = {(cuuint32_t)(128 / es), 128, 1, 1};
   cuuint32_t ones[4] = {1, 1, 1, 1};
-  return enc(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base),
+  return encode_tiled_cached(enc, m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base),
              dims, strides, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

@@ -861,7 +861,7 @@ bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ba
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  return enc(m, dt, rank, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+  return encode_tiled_cached(enc, m, dt, rank, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // [BH·Np][D] int8 rows, box D x 128, the swizzle of a D-byte row (128 B or 64 B)

@@ -3,10 +3,18 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <atomic>
 #include <cstdint>
 
 namespace sage3 {
+
+// cuTensorMapEncodeTiled through a per-process cache keyed by every argument (the descriptors of a repeated call —
+// same buffers, shapes and strides, the common case of a serving loop — are encoded once, abi.cu).
+CUresult encode_tiled_cached(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, CUtensorMapDataType dt,
+                             cuuint32_t rank, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                             const cuuint32_t* box, const cuuint32_t* es, CUtensorMapInterleave il,
+                             CUtensorMapSwizzle swz, CUtensorMapL2promotion promo, CUtensorMapFloatOOBfill oob);
 
 // Quantize workspace: the fp64 K chunk sums [BH][d][Np/128], then the fused K-mean control words (a work counter and
 // per head {chunk sums added, km ready}), zeroed by the launcher before each call.
