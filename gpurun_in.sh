@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_quant.py -q -p no:cacheprovider -k "fused" 2>&1 | tail -3 > gpurun_out/r2n_test.txt
+timeout 900 python tools/attn_ab.py build/lib_p2.so build/lib_qnew.so build/lib_p.so --reps 2 --shapes 32768:0,32768:1,8192:0,2048:0,1024:1 > gpurun_out/r2o_ab.txt 2>&1
