@@ -118,7 +118,7 @@ constexpr int kSBufs = 3;
 // TMEM columns per S/PV buffer (tile j -> kColRS + 16 (j % 3)); the ones operand's scale factors sit at kColSF1.
 constexpr uint32_t kColSF1 = 432, kColRS = 448;
 
-template <int D, bool kMX, bool kQSum = false, bool kPersist = false>
+template <int D, bool kMX, bool kQSum = false>
 struct Layout {
   static constexpr int kQKRow = D / 2;          // bytes per Q/K row (64 or 32)
   static constexpr int kQBytes = 128 * kQKRow;   // Q tile codes
@@ -144,15 +144,9 @@ struct Layout {
   // kQSum: the all-ones B operand (16 rows x 128 keys, E2M1 1.0 = code 2 in every nibble) and its SF atoms (E4M3 1.0)
   static constexpr int oOnes = ((oDs + kDsStages * 512 + 1023) / 1024) * 1024;
   static constexpr int oOnesSF = oOnes + 1024;
-  static constexpr int oEnd0 = kQSum ? oOnesSF + 1024 : oDs + kDsStages * 512;
-  // kPersist: a second Q slot (the next unit's Q̂ loads while the current unit runs) and a dedicated O staging
-  // buffer (the K/V rings are busy with the next unit when an epilogue runs), fp32-sized
-  static constexpr int oQ1 = ((oEnd0 + 1023) / 1024) * 1024;
-  static constexpr int oQSF1 = oQ1 + ((kQBytes + 1023) / 1024) * 1024;
-  static constexpr int oStage = ((oQSF1 + kQKSF + 1023) / 1024) * 1024;
-  static constexpr int oBar = kPersist ? oStage + D * 128 * 4 : oEnd0;
+  static constexpr int oBar = kQSum ? oOnesSF + 1024 : oDs + kDsStages * 512;
   static constexpr int kNumBars =
-      4 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages;
+      1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
@@ -165,21 +159,22 @@ struct Layout {
 // RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
 // of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
 // warpgroups are no longer independent in this mode.
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kPersist>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                     const AttnArgs a) {
-  using L = Layout<D, kMX, kQSum, kPersist>;
+  using L = Layout<D, kMX, kQSum>;
   extern __shared__ uint8_t smem_raw[];
   // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
   __shared__ __align__(1024) float2 s_lut[128];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
+  uint8_t* sQ = smem + L::oQ;
+  uint8_t* sQSF = smem + L::oQSF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
-  uint64_t* q_full = bars;       // [2]: Q̂ slot loaded (kPersist: unit ui uses slot ui % 2)
-  uint64_t* q_empty = bars + 2;  // [2]: kPersist: the S MMAs of the slot's unit are done with it
-  uint64_t* k_full = bars + 4;
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
   uint64_t* k_empty = k_full + kKStages;
   uint64_t* v_full = k_empty + kKStages;
   uint64_t* v_empty = v_full + kVStages;
@@ -198,33 +193,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Work unit u = unit_begin + blockIdx.x of the flattened (b·h, q-tile) space, q tiles fastest and in
   // descending order within a head (CTAs of one head run together and share K/V in L2; longest first under
   // causal masking).  sage3_attn_fwd covers every unit; the multi-GPU launcher gives each rank a range.
-  // kPersist (short sequences): grid = min(units, SMs) and CTA b processes units b, b + gridDim, ... one after the
-  // other; every role walks the same unit sequence and indexes its rings and TMEM buffers by the CTA's running KV
-  // tile count g (= g0 of the unit + j), so the pipelines run across unit boundaries (the next unit's Q̂ and first
-  // K/V tiles load while the current unit's epilogue runs).
   const int n_qt = a.Np >> 7;
-  const int64_t n_units = a.unit_end - a.unit_begin;
-  int bh = 0, qt = 0, nkv = 0;
-  auto unit_of = [&](int ui) {  // (bh, qt, nkv) of this CTA's unit ui; false past the last one
-    const int64_t u = (int64_t)blockIdx.x + (int64_t)ui * gridDim.x;
-    if ((!kPersist && ui > 0) || u >= n_units) return false;
-    const int64_t unit = a.unit_begin + u;
-    bh = (int)(unit / n_qt);
-    qt = n_qt - 1 - (int)(unit % n_qt);
-    nkv = a.causal ? qt + 1 : n_qt;
-    return true;
-  };
-  unit_of(0);
-  auto q_slot = [&](int ui) { return kPersist ? (ui & 1) : 0; };
-  auto sQ_of = [&](int qs) { return smem + (qs ? L::oQ1 : L::oQ); };
-  auto sQSF_of = [&](int qs) { return smem + (qs ? L::oQSF1 : L::oQSF); };
+  const int64_t unit = a.unit_begin + (int64_t)blockIdx.x;
+  const int bh = (int)(unit / n_qt);
+  const int qt = n_qt - 1 - (int)(unit % n_qt);
+  const int nkv = a.causal ? qt + 1 : n_qt;
 
   SAGE3_TRACE_EV(0, 127, 0);  // CTA start (thread 0)
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 1);
-    }
+    mbar_init(q_full, 1);
     for (int s = 0; s < kKStages; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -258,9 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // while the same code path costs 2-4% at N = 1K).
     if constexpr (kEarly) {
     const int row_q = bh * a.Np + qt * 128;
-    mbar_arrive_expect_tx(&q_full[0], L::kQBytes + L::kQKSF);
-    tma_load_2d(smem + L::oQ, &tm_q, &q_full[0], 0, row_q);
-    bulk_load(smem + L::oQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, &q_full[0]);
+    mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
+    tma_load_2d(smem + L::oQ, &tm_q, q_full, 0, row_q);
+    bulk_load(smem + L::oQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
     for (int j = 0; j < nkv && j < SAGE3_EARLY_K; ++j) {
       const int row_k = bh * a.Np + j * 128;
       mbar_arrive_expect_tx(&k_full[j], L::kKBytes + L::kQKSF);
@@ -295,48 +272,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer: Q, K
       if (elect_one()) {
-        for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
-          const bool early = kEarly && ui == 0;  // Q and K 0.. already requested in the prologue
-          const int qs = q_slot(ui);
-          if (!early) {
-            if (kPersist && ui >= 2) prod_wait(&q_empty[qs], ((uint32_t)((ui >> 1) - 1) & 1u));
-            const int row_q = bh * a.Np + qt * 128;
-            mbar_arrive_expect_tx(&q_full[qs], L::kQBytes + L::kQKSF);
-            tma_load_2d(sQ_of(qs), &tm_q, &q_full[qs], 0, row_q);
-            bulk_load(sQSF_of(qs), a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, &q_full[qs]);
-          }
-          for (int j = early ? SAGE3_EARLY_K : 0; j < nkv; ++j) {
-            const int g = g0 + j, st = g % kKStages;
-            const int row_k = bh * a.Np + j * 128;
-            prod_wait(&k_empty[st], ((uint32_t)(g / kKStages) & 1u) ^ 1u);
-            mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
-            tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
-            bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
-                      &k_full[st]);
-          }
+        constexpr bool early = kEarly;  // Q and K 0.. already requested in the prologue
+        if (!early) {
+          const int row_q = bh * a.Np + qt * 128;
+          mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
+          tma_load_2d(sQ, &tm_q, q_full, 0, row_q);
+          bulk_load(sQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
+        }
+        for (int j = early ? SAGE3_EARLY_K : 0; j < nkv; ++j) {
+          const int st = j % kKStages;
+          const int row_k = bh * a.Np + j * 128;
+          prod_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
+          tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
+          bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
+                    &k_full[st]);
         }
       }
       __syncwarp();
     } else if (warp == 3) {
       // ------------------------------------------------------------------ TMA producer: V
       if (elect_one()) {
-        for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
-          for (int j = 0; j < nkv; ++j) {
-            const int g = g0 + j;
-            if constexpr (kSQ) {  // ds[bh][qt][128 j .. 128 j + 128): the GEMV term of this (query, key) tile
-              const int ds_st = g % kDsStages;
-              prod_wait(&ds_empty[ds_st], ((uint32_t)(g / kDsStages) & 1u) ^ 1u);
-              mbar_arrive_expect_tx(&ds_full[ds_st], 512);
-              bulk_load(smem + L::oDs + ds_st * 512, a.ds + ((int64_t)bh * n_qt + qt) * a.Np + j * 128, 512,
-                        &ds_full[ds_st]);
-            }
-            const int st = g % kVStages;
-            prod_wait(&v_empty[st], ((uint32_t)(g / kVStages) & 1u) ^ 1u);
-            mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
-            tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
-            bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
-                      &v_full[st]);
+        for (int j = 0; j < nkv; ++j) {
+          if constexpr (kSQ) {  // ds[bh][qt][128 j .. 128 j + 128): the GEMV term of this (query, key) tile
+            const int ds_st = j % kDsStages;
+            prod_wait(&ds_empty[ds_st], ((uint32_t)(j / kDsStages) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&ds_full[ds_st], 512);
+            bulk_load(smem + L::oDs + ds_st * 512, a.ds + ((int64_t)bh * n_qt + qt) * a.Np + j * 128, 512,
+                      &ds_full[ds_st]);
           }
+          const int st = j % kVStages;
+          prod_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
+          tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
+          bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
+                    &v_full[st]);
         }
       }
       __syncwarp();
@@ -355,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             mma_nvf4(d, ad, bd, make_idesc_nvf4(128, n), sfa + 4 * ks, sfb + 4 * ks, ks > 0);
         };
-        auto issue_s = [&](int j, const uint8_t* sQ) {  // j: the CTA's running tile count g
+        auto issue_s = [&](int j) {
           const int b = j % kSBufs, st = j % kKStages;
           SAGE3_TRACE_EV(5, j, 0);
           mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
@@ -415,24 +385,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           SAGE3_TRACE_EV(6, j, 3);
         };
         if (warp == 1) {
-          for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
-            const int qs = q_slot(ui);
-            mbar_wait(&q_full[qs], kPersist ? (uint32_t)((ui >> 1) & 1) : 0u);
-            tc_fence_after();
+          mbar_wait(q_full, 0);
+          tc_fence_after();
 #pragma unroll
-            for (int at = 0; at < kQKAtoms; ++at)
-              tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * at, sf_desc(sQSF_of(qs) + 512 * at));
-            for (int j = 0; j < nkv; ++j) issue_s(g0 + j, sQ_of(qs));  // S into buffer g%3 once it is free
-            if constexpr (kPersist) mma_commit(&q_empty[qs]);      // the slot's S MMAs are issued: reusable
-          }
+          for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * at, sf_desc(sQSF + 512 * at));
+          for (int j = 0; j < nkv; ++j) issue_s(j);  // S_j into buffer j%3 once the correction freed it
         } else {
           if constexpr (kQSum) {
 #pragma unroll
             for (int at = 0; at < 2; ++at)
               tmem_cp_32x128b_x4(tbase + kColSF1 + 4 * at, sf_desc(smem + L::oOnesSF + 512 * at));
           }
-          for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui)
-            for (int j = 0; j < nkv; ++j) issue_pv(g0 + j);
+          for (int j = 0; j < nkv; ++j) issue_pv(j);
         }
       }
       __syncwarp();
@@ -440,9 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (wg >= 2) {
     // -------------------------------------------------------------------- softmax + two-level P quant
     setmaxnreg_inc<reg_softmax<D>()>();
-    const int par = wg - 2;                 // this warpgroup's KV-tile parity (of the running tile count g)
+    const int par = wg - 2;                 // this warpgroup's KV-tile parity
     const int r = threadIdx.x - 128 * wg;   // query row in the tile == TMEM lane
-    int q_row = qt * 128 + r;
+    const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = a.scale * kLog2e;
     const f2 sl2x2 = make_float2(sl2, sl2);
@@ -450,14 +414,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // One KV tile (Alg1 L8-L10 for this warpgroup's rows).  Only the last tile can need masking (keys >= N,
     // or the causal diagonal), so it is a separate instantiation outside the hot loop: the loop body is
     // straight-line code with no masking branches (instruction-cache friendly).
-    auto tile = [&](const int j, const int g, auto masked_tag) {  // j: KV tile of the unit, g: running count
+    auto tile = [&](const int j, auto masked_tag) {
       constexpr bool masked = decltype(masked_tag)::value;
-      const int sb = g % kSBufs, pb = g % kPBufs;
+      const int sb = j % kSBufs, pb = j % kPBufs;
       const uint32_t s_addr = lane_base + 128 * sb;
       const uint32_t sP = smem_u32(smem + L::oP + pb * L::kPBytes) + r * 64;
       const uint32_t sPSF = smem_u32(smem + L::oPSF + pb * L::kPSF) + (r & 31) * 16 + (r >> 5) * 4;
       SAGE3_TRACE_EV(1 + par, j, 0);
-      mbar_wait(&s_full[sb], (uint32_t)(g / kSBufs) & 1u);
+      mbar_wait(&s_full[sb], (uint32_t)(j / kSBufs) & 1u);
       SAGE3_TRACE_EV(1 + par, j, 1);
       tc_fence_after();
       const int kv0 = j * 128;
@@ -469,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
         if constexpr (kSQ) {  // Alg1 L8: S += GEMV(q̄_i, K_j^T), the same 128-vector for every row (broadcast)
-          const uint32_t ds_s = smem_u32(smem + L::oDs + (g % kDsStages) * 512) + c * 128;
+          const uint32_t ds_s = smem_u32(smem + L::oDs + (j % kDsStages) * 512) + c * 128;
 #pragma unroll
           for (int t = 0; t < 32; t += 4) {
             float4 g;
@@ -487,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
       };
-      if constexpr (kSQ) mbar_wait(&ds_full[g % kDsStages], (uint32_t)(g / kDsStages) & 1u);
+      if constexpr (kSQ) mbar_wait(&ds_full[j % kDsStages], (uint32_t)(j / kDsStages) & 1u);
       if constexpr (kSQ) {  // two loads in flight (the ds chunk needs registers too)
         uint32_t va[32], vb[32];
 #pragma unroll
@@ -500,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pass1(c + 1, vb);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_empty[g % kDsStages]);  // ds slot read by this warp
+        if (lane == 0) mbar_arrive(&ds_empty[j % kDsStages]);  // ds slot read by this warp
       } else {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
         uint32_t va[32], vb[32], vc[32], vd[32];
         tmem_ld_32x32b_x32(s_addr, va);
@@ -520,15 +484,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
       SAGE3_TRACE_EV(par ? 3 : 0, j, 2);
-      const int slot = g % kXSlots;
+      const int slot = j % kXSlots;
       // the exponent reference of this tile's values: tmax_j (two-level: P̃2 = 2688·2^{sl2(S - tmax_j)}) or the
       // running max m_j (direct: P̃ = 2^{sl2(S - m_j)}); the correction warpgroup weights the tile by it
       float eref = tmax;
       if constexpr (kDirect) {
         float mp = -INFINITY;
         if (j > 0) {
-          const int ps = (g - 1) % kXSlots;
-          mbar_wait(&m_full[ps], (uint32_t)((g - 1) / kXSlots) & 1u);
+          const int ps = (j - 1) % kXSlots;
+          mbar_wait(&m_full[ps], (uint32_t)((j - 1) / kXSlots) & 1u);
           mp = lds_f32(xchg_s + ps * 1024);
         }
         eref = fmaxf(mp, tmax);
@@ -581,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       SAGE3_TRACE_EV(par ? 3 : 0, j, 4);
       SAGE3_TRACE_EV(1 + par, j, 2);
-      mbar_wait(&p_empty[pb], ((uint32_t)(g / kPBufs) & 1u) ^ 1u);
+      mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
       SAGE3_TRACE_EV(1 + par, j, 3);
       // ---- pass 2: y = P̃2/s, codes E2M1(y), rowsum(P̃2) = Σ_blk s_blk·Σy.  Software-pipelined over the four
       //      32-key chunks: the exp2 of chunk c (MUFU / FMA-pipe polynomial) sits in the same straight-line
@@ -665,17 +629,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       SAGE3_TRACE_WARP(1 + par, j, 4);
     };
-    for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
-      q_row = qt * 128 + r;
-      const int last = nkv - 1;
-      const bool last_masked = last * 128 + 128 > a.N || a.causal;
-      for (int j = ((g0 & 1) == par) ? 0 : 1; j < last; j += 2) tile(j, g0 + j, std::false_type{});
-      if (((g0 + last) & 1) == par) {
-        if (last_masked)
-          tile(last, g0 + last, std::true_type{});
-        else
-          tile(last, g0 + last, std::false_type{});
-      }
+    const int last = nkv - 1;
+    const bool last_masked = last * 128 + 128 > a.N || a.causal;
+    for (int j = par; j < last; j += 2) tile(j, std::false_type{});
+    if ((last & 1) == par) {
+      if (last_masked)
+        tile(last, std::true_type{});
+      else
+        tile(last, std::false_type{});
     }
   } else {
     // -------------------------------------------------------------------- correction + epilogue
@@ -685,22 +646,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     // which is Alg1 L9-L11 up to fp32 rounding: O/l and lse are independent of the reference.
     setmaxnreg_inc<reg_correction<D>()>();
     const int r = threadIdx.x - 128;
+    const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     [[maybe_unused]] const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
     const float sl2 = a.scale * kLog2e;
-    f2 o[D / 2];
-    for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
-    const int q_row = qt * 128 + r;
     float mref = -INFINITY, l = 0.0f;
+    f2 o[D / 2];
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) o[c] = make_float2(0.f, 0.f);
     for (int j = 0; j < nkv; ++j) {
-      const int g = g0 + j;
-      const int slot = g % kXSlots, b = g % kSBufs;
+      const int slot = j % kXSlots, b = j % kSBufs;
       SAGE3_TRACE_EV(4, j, 0);
 #if SAGE3_XCHG_TMEM
       SAGE3_TRACE_EV(4, j, 1);
-      mbar_wait(&pv_full[b], (uint32_t)(g / kSBufs) & 1u);
+      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
       uint32_t xv[2];
@@ -710,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = __uint_as_float(xv[0]);
       const float rs2 = __uint_as_float(xv[1]);
 #else
-      mbar_wait(&x_full[slot], (uint32_t)(g / kXSlots) & 1u);
+      mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
       SAGE3_TRACE_EV(4, j, 1);
       const float tmax = lds_f32(xchg_s + slot * 1024);
       const float rs2 = lds_f32(xchg_s + slot * 1024 + 512);
@@ -729,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!kQSum) l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
 #if !SAGE3_XCHG_TMEM
-      mbar_wait(&pv_full[b], (uint32_t)(g / kSBufs) & 1u);
+      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
 #endif
@@ -786,17 +745,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
     SAGE3_TRACE_EV(4, 126, 1);
-    // coalesced store: rows -> smem (the K/V rings, idle once the last PV MMA has completed; kPersist: the
-    // dedicated staging buffer, the rings already hold the next unit's tiles) -> TMA
-    uint8_t* stage = smem + (kPersist ? L::oStage : L::oK);
+    // coalesced store: rows -> smem (the K/V rings, idle once the last PV MMA has completed) -> TMA
+    uint8_t* stage = smem + L::oK;
     stage_o_row<D>(stage, r, a.o_dtype, o);
     SAGE3_TRACE_EV(4, 126, 2);
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     SAGE3_TRACE_EV(4, 126, 3);
     if (threadIdx.x == 128) store_o_tile<D>(&tm_o, stage, a.o_dtype, qt * 128, bh % a.H, bh / a.H);
-    if constexpr (kPersist) named_bar_sync(1, 128);  // the store has read the staging buffer (thread 128 waited)
-    }
   }
   SAGE3_TRACE_EV(4, 127, 2);  // correction: epilogue stores issued (thread 128)
   tc_fence_before();
@@ -809,18 +765,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------- host
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kPersist>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
 cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D, kMX, kQSum, kPersist>;
+  using L = Layout<D, kMX, kQSum>;
   static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)
-  static int n_sm[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum, kPersist>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
     if (e != cudaSuccess) return e;
-    cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
     attr_done[dev] = true;
   }
   const int BH = a.B * a.H;
@@ -832,26 +785,16 @@ cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  const int64_t sms = dev < 64 && n_sm[dev] > 0 ? n_sm[dev] : 148;
-  const unsigned grid = (unsigned)(kPersist ? (units < sms ? units : sms) : units);
-  attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum, kPersist><<<grid, kThreads, L::kSmemAlloc, stream>>>(
-      tq, tk, tv, to, a);
+  attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
   return cudaGetLastError();
 }
 
-#ifndef SAGE3_PERSIST_MAX_N
-#define SAGE3_PERSIST_MAX_N 2048  // sequences up to this long run the persistent instantiation (0: never)
-#endif
 template <int D, bool kSQ, bool kMX, bool kDirect, bool kQSum = false>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
-  if constexpr (!kSQ && !kDirect && !kMX) {
-    // short sequences: persistent CTAs (a unit's prologue and epilogue overlap its neighbours' work)
-    if (a.N <= SAGE3_PERSIST_MAX_N) return launch_dk<D, kSQ, kMX, kDirect, false, kQSum, true>(a, stream);
-  }
   if constexpr (!kSQ && !kDirect) {  // the north_star path: long sequences take the early-TMA instantiation
-    if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true, kQSum, false>(a, stream);
+    if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true, kQSum>(a, stream);
   }
-  return launch_dk<D, kSQ, kMX, kDirect, false, kQSum, false>(a, stream);
+  return launch_dk<D, kSQ, kMX, kDirect, false, kQSum>(a, stream);
 }
 
 }  // namespace
