@@ -9,11 +9,11 @@
 //                  PV_j = FP4MM(P̂2_j, s_P2, V̂_j, s_V)    M=128 N=d K=128, written over S_j's TMEM columns
 //                scale factors go smem -> TMEM with tcgen05.cp.32x128b.warpx4, in MMA issue order
 //       warp 2   TMEM allocator (512 columns)
-//   WG1, WG2     softmax + two-level P quantization, one query row per thread (TMEM lane = row);
-//                WG1 takes the even KV tiles (S buffer 0), WG2 the odd ones (S buffer 1).  A tile's P̂2
+//   WG2, WG3     softmax + two-level P quantization, one query row per thread (TMEM lane = row);
+//                WG2 takes the even KV tiles, WG3 the odd ones.  A tile's P̂2
 //                codes and s_P2 depend only on that tile's row max (see below), so the two warpgroups
 //                never synchronise with each other.
-//   WG3          correction: owns the online-softmax recurrence (m, l; Alg1 L9) and O in registers:
+//   WG1          correction: owns the online-softmax recurrence (m, l; Alg1 L9) and O in registers:
 //                O = α·O + s_P1·PV_j (Alg1 L11), then O/l (L13) and the store.
 //
 // Two-level P in tile-local form (reading c14): with tmax_j = rowmax(S_ij),
