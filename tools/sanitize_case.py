@@ -1,6 +1,6 @@
 """Small end-to-end cases for compute-sanitizer (SURVEY §4 layer 7): quantize + attention (d 64/128, causal
-and not, ragged N, smoothing Q, MXFP4, direct and lazy P, SageBwd INT8 forward and backward) through the C ABI, plus the
-host-buffer path.
+and not, ragged N, smoothing Q, MXFP4, direct, lazy and qsum P, SageBwd INT8 forward and backward) through the C ABI,
+plus the host-buffer path.  With SAGE3_QUANT_FUSED_K=1 in the environment the quantizer runs its fused K-mean path.
   compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_case.py"""
 import os
 import sys
@@ -21,6 +21,7 @@ for d in (64, 128):
             s3.attention(Q, K, V, causal=causal, p_quant="direct")
             s3.attention(Q, K, V, causal=causal, p_quant="lazy")
             s3.attention(Q, K, V, causal=causal, fmt="mxfp4", p_quant="lazy")
+            s3.attention(Q, K, V, causal=causal, p_quant="qsum")  # round 2: the row-sum variant
             qkv8 = s3.sage3_int8_quantize_qkv(Q, K, V)
             lse = torch.empty(1, 1, N, dtype=torch.float32, device="cuda")
             O8 = s3.sage3_int8_attn_fwd(qkv8, causal=causal, lse=lse)
