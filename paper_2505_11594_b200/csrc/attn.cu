@@ -59,9 +59,6 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_XCHG_TMEM
 #define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
 #endif
-#ifndef SAGE3_XPIPE
-#define SAGE3_XPIPE 0  // 1: cross-tile software pipelining in the softmax warps (pass 1 of tile j+2 inside pass 2 of j)
-#endif
 #ifndef SAGE3_PROD_BACKOFF
 #define SAGE3_PROD_BACKOFF 0  // 1: TMA producers poll their empty barriers with test_wait + timed sleep
 #endif
@@ -634,168 +631,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     const int last = nkv - 1;
     const bool last_masked = last * 128 + 128 > a.N || a.causal;
-    constexpr bool kXPipe = SAGE3_XPIPE && !kSQ && !kDirect && !kMX;
-    if constexpr (kXPipe) {
-      // ---- cross-tile software pipeline: pass 1 (TMEM loads + 16-key block maxima) of this warpgroup's next tile
-      //      j+2 runs inside pass 2 of tile j (chunks 2-3), hiding its latency behind pass 2's MUFU / FMA work.
-      //      Same arithmetic as `tile` (two-level, tile-local form); a masked (last) tile is not interleaved.
-      //      y = P̃2/s is computed in place over the S registers of its chunk (register budget).
-      auto scales = [&](const float (&bmax)[8], float& tmax, float (&nbb)[8], float (&sdec)[8], uint32_t (&scw)[2]) {
-        tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]), fmaxf(bmax[6], bmax[7]));
-        const float nb = kLog2_2688 - tmax * sl2;
-        uint32_t c2[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const f2 e = ffma2(make_float2(bmax[2 * k], bmax[2 * k + 1]), sl2x2, make_float2(nb, nb));
-          const f2 q = fmul2(make_float2(ex2(e.x), ex2(e.y)), make_float2(kOneSixth, kOneSixth));
-          c2[k] = cvt_e4m3x2(q.x, q.y);
-        }
-        scw[0] = __byte_perm(c2[0], c2[1], 0x5410);
-        scw[1] = __byte_perm(c2[2], c2[3], 0x5410);
-#pragma unroll
-        for (int blk = 0; blk < 8; ++blk) {
-          const float2 t = s_lut[(scw[blk >> 2] >> (8 * (blk & 3))) & 0xFFu];
-          nbb[blk] = nb + t.x;
-          sdec[blk] = t.y;
-        }
-      };
-      // pass 1 of tile j on its own (all four loads in flight); masked: keys past `lim` set to -inf in TMEM
-      auto pass1_full = [&](int j, bool masked, float (&bmax)[8]) {
-        const uint32_t s_addr = lane_base + 128 * (j % kSBufs);
-        mbar_wait(&s_full[j % kSBufs], (uint32_t)(j / kSBufs) & 1u);
-        tc_fence_after();
-        const int lim = a.causal ? min(a.N - 1, q_row) - j * 128 : a.N - 1 - j * 128;
-        uint32_t v[4][32];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_addr + 32 * c, v[c]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld_wait_regs(v[c]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float* f = reinterpret_cast<float*>(v[c]);
-          if (masked) {
-#pragma unroll
-            for (int t = 0; t < 32; ++t) f[t] = (32 * c + t > lim) ? -INFINITY : f[t];
-            tmem_st_32x32b_x32(s_addr + 32 * c, v[c]);
-          }
-          bmax[2 * c] = max16(f);
-          bmax[2 * c + 1] = max16(f + 16);
-        }
-        if (masked) tmem_st_wait();
-      };
-      // pass-2 chunk c of tile j: y in place, E2M1 codes -> smem, rowsum share
-      auto chunk2 = [&](int c, uint32_t (&v)[32], const float (&nbb)[8], const float (&sdec)[8], uint32_t sP,
-                        float& rowsum) {
-        const float nA = nbb[2 * c], nB = nbb[2 * c + 1];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float nbh = i < 8 ? nA : nB;
-          const f2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2,
-                             make_float2(nbh, nbh));
-          const f2 y = ((poly_mask<kQSum>() >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          v[2 * i] = __float_as_uint(y.x);
-          v[2 * i + 1] = __float_as_uint(y.y);
-        }
-        const f2* yy0 = reinterpret_cast<const f2*>(v);
-        uint32_t w[4];
-#pragma unroll
-        for (int hb = 0; hb < 2; ++hb) {
-          const f2* yy = yy0 + 8 * hb;
-          if constexpr (!kQSum) {
-            const f2 s01 = fadd2(fadd2(yy[0], yy[1]), fadd2(yy[2], yy[3]));
-            const f2 s23 = fadd2(fadd2(yy[4], yy[5]), fadd2(yy[6], yy[7]));
-            const f2 sy = fadd2(s01, s23);
-            rowsum = fmaf(sdec[2 * c + hb], sy.x + sy.y, rowsum);
-          }
-          w[2 * hb] = cvt_e2m1x8(yy[0].x, yy[0].y, yy[1].x, yy[1].y, yy[2].x, yy[2].y, yy[3].x, yy[3].y);
-          w[2 * hb + 1] = cvt_e2m1x8(yy[4].x, yy[4].y, yy[5].x, yy[5].y, yy[6].x, yy[6].y, yy[7].x, yy[7].y);
-        }
-        sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
-      };
-      auto finalize = [&](int j, float tmax, float rowsum, const uint32_t (&scw)[2]) {
-        const int pb = j % kPBufs, slot = j % kXSlots;
-        const uint32_t sPSF = smem_u32(smem + L::oPSF + pb * L::kPSF) + (r & 31) * 16 + (r >> 5) * 4;
-        sts_u32(sPSF, scw[0]);
-        sts_u32(sPSF + 512, scw[1]);
-        sts_f32(xchg_s + slot * 1024, tmax);
-        sts_f32(xchg_s + slot * 1024 + 512, rowsum);
-        tc_fence_before();
-        fence_proxy_async_smem();
-        mbar_arrive(&x_full[slot]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[pb]);
-      };
-      int cur = par;
-      if (cur <= last) {
-        float bmax[8], tmax, nbb[8], sdec[8];
-        uint32_t scw[2];
-        pass1_full(cur, cur == last && last_masked, bmax);
-        scales(bmax, tmax, nbb, sdec, scw);
-        for (;;) {
-          const int nxt = cur + 2;
-          const bool inter = nxt < last || (nxt == last && !last_masked);  // interleave the next tile's pass 1
-          const uint32_t s_cur = lane_base + 128 * (cur % kSBufs);
-          const uint32_t sP = smem_u32(smem + L::oP + (cur % kPBufs) * L::kPBytes) + r * 64;
-          mbar_wait(&p_empty[cur % kPBufs], ((uint32_t)(cur / kPBufs) & 1u) ^ 1u);
-          float rowsum = 0.0f;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(s_cur + 32 * c, v);
-            tmem_ld_wait_regs(v);
-            chunk2(c, v, nbb, sdec, sP, rowsum);
-          }
-          float bn[8];
-          if (inter) {
-            const uint32_t s_nxt = lane_base + 128 * (nxt % kSBufs);
-            mbar_wait(&s_full[nxt % kSBufs], (uint32_t)(nxt / kSBufs) & 1u);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 2; c < 4; ++c) {  // pass-2 chunk c of cur with pass-1 chunks 2(c-2), 2(c-2)+1 of nxt
-              uint32_t v[32], u0[32], u1[32];
-              tmem_ld_32x32b_x32(s_cur + 32 * c, v);
-              tmem_ld_32x32b_x32(s_nxt + 64 * (c - 2), u0);
-              tmem_ld_32x32b_x32(s_nxt + 64 * (c - 2) + 32, u1);
-              tmem_ld_wait_regs(v);
-              tmem_ld_wait_regs(u0);
-              tmem_ld_wait_regs(u1);
-              const float* f0 = reinterpret_cast<const float*>(u0);
-              const float* f1 = reinterpret_cast<const float*>(u1);
-              bn[4 * (c - 2)] = max16(f0);
-              bn[4 * (c - 2) + 1] = max16(f0 + 16);
-              bn[4 * (c - 2) + 2] = max16(f1);
-              bn[4 * (c - 2) + 3] = max16(f1 + 16);
-              chunk2(c, v, nbb, sdec, sP, rowsum);
-            }
-          } else {
-#pragma unroll
-            for (int c = 2; c < 4; ++c) {
-              uint32_t v[32];
-              tmem_ld_32x32b_x32(s_cur + 32 * c, v);
-              tmem_ld_wait_regs(v);
-              chunk2(c, v, nbb, sdec, sP, rowsum);
-            }
-          }
-          finalize(cur, tmax, rowsum, scw);
-          if (nxt > last) break;
-          if (inter) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) bmax[k] = bn[k];
-          } else {
-            pass1_full(nxt, nxt == last && last_masked, bmax);
-          }
-          scales(bmax, tmax, nbb, sdec, scw);
-          cur = nxt;
-        }
-      }
-    } else {
     for (int j = par; j < last; j += 2) tile(j, std::false_type{});
     if ((last & 1) == par) {
       if (last_masked)
         tile(last, std::true_type{});
       else
         tile(last, std::false_type{});
-    }
     }
   } else {
     // -------------------------------------------------------------------- correction + epilogue
