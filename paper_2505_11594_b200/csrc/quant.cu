@@ -1,6 +1,6 @@
 // quant.cu — sm_100a kernels for sage3_quantize_qkv: smoothing K (Alg1 L2) and NVFP4
 // microscaling φ (Eq. 1) of Q, K (1x16 blocks along d) and V (1x16 blocks along tokens, written
-// transposed).  HBM-bound: K-mean sums (4-byte coalesced loads, fp64) + their fixed-order reduction,
+// transposed).  HBM-bound: K-mean sums (16-byte coalesced loads, fp64) + their fixed-order reduction,
 // then one persistent streaming kernel (TMA tiles -> smem ring -> φ) over all Q, Vᵀ and K chunks.
 //
 // MXFP4 (Tab1a ablation, template kMX): blocks of 32 with E8M0 scales (e8m0_ceil in sm100.cuh, reading c11).
@@ -83,39 +83,42 @@ __device__ __forceinline__ uint32_t codes8(const float* x, float rs) {
 }
 
 // ---------------------------------------------------------------------------------- K mean
-// grid (Np/128, B*H), block d/2: thread t sums channels 2t, 2t+1 over one 128-token chunk in ascending token
-// order (fp64, sequential; 4-byte loads, a warp reads 128 contiguous bytes of a token row), writes
-// ws[bh][chunk][c]; kmean_final_kernel then reduces the chunk sums (reading c10).
+// grid (ceil(Np/128 / 8), B*H), block 8·d/8 threads: a group of d/8 threads per 128-token chunk (8 chunks per
+// block), thread t of a group sums channels 8t .. 8t+7 over the chunk in ascending token order (fp64, sequential,
+// reading c10) from one 16-byte load per token row (the group reads a contiguous 2·d-byte row segment), and writes
+// ws[bh][channel][chunk]; kmean_final_kernel then reduces the chunk sums in ascending chunk order.
 template <typename T>
-__global__ void __launch_bounds__(64) kmean_kernel(const T* __restrict__ k, int64_t sb, int64_t sh, int64_t sn,
-                                                   int H, int N, int d, double* __restrict__ ws) {
-  const int chunk = blockIdx.x, bh = blockIdx.y;
+__global__ void __launch_bounds__(128) kmean_kernel(const T* __restrict__ k, int64_t sb, int64_t sh, int64_t sn,
+                                                    int H, int N, int d, int nch, double* __restrict__ ws) {
+  const int per = d / 8;  // threads per chunk
+  const int chunk = blockIdx.x * (128 / per) + threadIdx.x / per, bh = blockIdx.y;
+  if (chunk >= nch) return;
   const int b = bh / H, h = bh % H;
-  const int c = threadIdx.x * 2;
+  const int c = (threadIdx.x % per) * 8;
   const T* base = k + b * sb + h * sh + c;
   const int n0 = chunk * 128, n1 = min(n0 + 128, N);
-  double a0 = 0.0, a1 = 0.0;
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int n = n0;
-  for (; n + 8 <= n1; n += 8) {
-    uint32_t v[8];
+  for (; n + 4 <= n1; n += 4) {
+    uint4 v[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)(n + i) * sn));
+    for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)(n + i) * sn));
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const T* p = reinterpret_cast<const T*>(&v[i]);
-      a0 += (double)to_f32<T>(p[0]);
-      a1 += (double)to_f32<T>(p[1]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += (double)to_f32<T>(p[e]);
     }
   }
   for (; n < n1; ++n) {
-    const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)n * sn));
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)n * sn));
     const T* p = reinterpret_cast<const T*>(&v);
-    a0 += (double)to_f32<T>(p[0]);
-    a1 += (double)to_f32<T>(p[1]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += (double)to_f32<T>(p[e]);
   }
-  double* out = ws + ((int64_t)bh * d + c) * gridDim.x + chunk;  // [bh][channel][chunk]
-  out[0] = a0;
-  out[gridDim.x] = a1;
+  double* out = ws + ((int64_t)bh * d + c) * nch + chunk;  // [bh][channel][chunk]
+#pragma unroll
+  for (int e = 0; e < 8; ++e) out[(int64_t)e * nch] = acc[e];
 }
 
 // One warp per (bh, channel): lane l loads chunk sums 8l..8l+7 (the channel's sums are contiguous:
@@ -666,8 +669,8 @@ cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t 
     if (e != cudaSuccess) return e;
     quant_stream_kernel<T, D, kMX, true><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v, ip, ws, ctl);
   } else {
-    kmean_kernel<T><<<grid, D / 2, 0, stream>>>(reinterpret_cast<const T*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn, qk.H,
-                                                qk.N, D, ws);
+    kmean_kernel<T><<<dim3((nch * (D / 8) + 127) / 128, BH), 128, 0, stream>>>(
+        reinterpret_cast<const T*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn, qk.H, qk.N, D, nch, ws);
     kmean_final_kernel<<<(BH * D * 32 + 255) / 256, 256, 0, stream>>>(ws, nch, qk.N, BH * D, qk.k_mean);
     quant_stream_kernel<T, D, kMX, false><<<ctas, 288, L::kAlloc, stream>>>(tq, tk, tv, qk, v, ip, ws, ctl);
   }
@@ -699,12 +702,14 @@ cudaError_t launch_fmt(const QKArgs& qk, const VArgs& v, bool bf16, double* ws, 
 cudaError_t launch_kmean(const QKArgs& qk, bool bf16, double* ws, cudaStream_t stream) {
   const int BH = qk.B * qk.H;
   dim3 grid(qk.Np / 128, BH);
+  const int nch = qk.Np / 128;
+  const dim3 kgrid((nch * (qk.d / 8) + 127) / 128, BH);
   if (bf16)
-    kmean_kernel<__nv_bfloat16><<<grid, qk.d / 2, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(qk.k), qk.k_sb,
-                                                                qk.k_sh, qk.k_sn, qk.H, qk.N, qk.d, ws);
+    kmean_kernel<__nv_bfloat16><<<kgrid, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(qk.k), qk.k_sb,
+                                                           qk.k_sh, qk.k_sn, qk.H, qk.N, qk.d, nch, ws);
   else
-    kmean_kernel<__half><<<grid, qk.d / 2, 0, stream>>>(reinterpret_cast<const __half*>(qk.k), qk.k_sb, qk.k_sh,
-                                                         qk.k_sn, qk.H, qk.N, qk.d, ws);
+    kmean_kernel<__half><<<kgrid, 128, 0, stream>>>(reinterpret_cast<const __half*>(qk.k), qk.k_sb, qk.k_sh, qk.k_sn,
+                                                    qk.H, qk.N, qk.d, nch, ws);
   kmean_final_kernel<<<(BH * qk.d * 32 + 255) / 256, 256, 0, stream>>>(ws, qk.Np / 128, qk.N, BH * qk.d, qk.k_mean);
   return cudaGetLastError();
 }
