@@ -347,6 +347,9 @@ def main():
     multigpu.self_launch(args.gpus, sys.argv[1:], os.path.abspath(__file__))
     import paper_2505_11594_b200 as s3
 
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:  # NCCL's init log (transport, NVLS) on stderr, for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     rank, world, local = multigpu.init_from_env("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
