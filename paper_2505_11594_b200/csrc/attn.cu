@@ -84,6 +84,7 @@ constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
 constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
+constexpr int kDsOps = 3;     // smoothing Q: tf32 B operands of the ds MMA (tile j -> j % 3)
 constexpr int kThreads = 512;
 // Per-thread register budgets after setmaxnreg (one warp of each warpgroup per SM sub-partition:
 // kRegWG0 + 2 kRegSoftmax + kRegCorrection = 512 = 64K registers / 128 lanes).
@@ -118,7 +119,7 @@ constexpr int kSBufs = 3;
 // TMEM columns per S/PV buffer (tile j -> kColRS + 16 (j % 3)); the ones operand's scale factors sit at kColSF1.
 constexpr uint32_t kColSF1 = 432, kColRS = 448;
 
-template <int D, bool kMX, bool kQSum = false>
+template <int D, bool kMX, bool kQSum = false, bool kSQ = false>
 struct Layout {
   static constexpr int kQKRow = D / 2;          // bytes per Q/K row (64 or 32)
   static constexpr int kQBytes = 128 * kQKRow;   // Q tile codes
@@ -144,9 +145,13 @@ struct Layout {
   // kQSum: the all-ones B operand (16 rows x 128 keys, E2M1 1.0 = code 2 in every nibble) and its SF atoms (E4M3 1.0)
   static constexpr int oOnes = ((oDs + kDsStages * 512 + 1023) / 1024) * 1024;
   static constexpr int oOnesSF = oOnes + 1024;
-  static constexpr int oBar = kQSum ? oOnesSF + 1024 : oDs + kDsStages * 512;
+  // kSQ: the tf32 operands of the ds MMA (S += 1·dsᵀ): A = 128 identical rows [1,1,1,0, 1,1,1,0] (4 KB), and
+  // kDsOps B slots of 128 keys x 8 tf32 (32 B per key: [hi, mid, lo, 0] of ds in one 16-byte half, zeros in the other)
+  static constexpr int oDsOne = oOnes;
+  static constexpr int oDsOp = oDsOne + 4096;
+  static constexpr int oBar = kQSum ? oOnesSF + 1024 : kSQ ? oDsOp + kDsOps * 4096 : oDs + kDsStages * 512;
   static constexpr int kNumBars =
-      1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages;
+      1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages + 2 * kDsOps;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                     const AttnArgs a) {
-  using L = Layout<D, kMX, kQSum>;
+  using L = Layout<D, kMX, kQSum, kSQ>;
   extern __shared__ uint8_t smem_raw[];
   // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
   __shared__ __align__(1024) float2 s_lut[128];
@@ -184,9 +189,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = b_empty + kSBufs;    // softmax -> MMA: P̂2_j / s_P2 in smem buffer j%4, S_j consumed
   uint64_t* p_empty = p_full + kPBufs;    // MMA -> softmax: PV_j done with smem buffer j%4
   uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8 (smem mode)
-  uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (TMA)
-  uint64_t* ds_empty = ds_full + kDsStages;  // softmax -> V producer: slot read
+  uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (bulk copy)
+  uint64_t* ds_empty = ds_full + kDsStages;  // (unused)
   uint64_t* m_full = ds_empty + kDsStages;    // direct P: m_j of tile j in xchg slot j%8 (softmax -> softmax)
+  uint64_t* dsop_full = m_full + kXSlots;     // smoothing Q: V-producer warp -> MMA: tf32 ds operand of tile j in slot j%3
+  uint64_t* dsop_empty = dsop_full + kDsOps;  // MMA -> V-producer warp: the ds MMA of tile j read slot j%3
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -223,7 +230,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kXSlots; ++s) mbar_init(&m_full[s], 128);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
-      mbar_init(&ds_empty[s], 4);  // one arrival per softmax warp of the tile's warpgroup
+      mbar_init(&ds_empty[s], 1);
+    }
+    for (int s = 0; s < kDsOps; ++s) {
+      mbar_init(&dsop_full[s], 1);
+      mbar_init(&dsop_empty[s], 1);
     }
     fence_mbar_init();
     prefetch_tmap(&tm_q);
@@ -260,6 +271,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = threadIdx.x; i < 512; i += kThreads) ones[i] = i < 256 ? 0x22222222u : 0x38383838u;
     fence_proxy_async_smem();
   }
+  if constexpr (kSQ) {  // the ds MMA's constant A operand (rows [1,1,1,0, 1,1,1,0]) and zeroed B slots
+    uint32_t* one = reinterpret_cast<uint32_t*>(smem + L::oDsOne);
+    for (int i = threadIdx.x; i < 1024; i += kThreads) one[i] = (i & 3) == 3 ? 0u : 0x3F800000u;
+    uint32_t* op = reinterpret_cast<uint32_t*>(smem + L::oDsOp);
+    for (int i = threadIdx.x; i < kDsOps * 1024; i += kThreads) op[i] = 0u;
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -291,16 +309,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     } else if (warp == 3) {
-      // ------------------------------------------------------------------ TMA producer: V
-      if (elect_one()) {
-        for (int j = 0; j < nkv; ++j) {
-          if constexpr (kSQ) {  // ds[bh][qt][128 j .. 128 j + 128): the GEMV term of this (query, key) tile
-            const int ds_st = j % kDsStages;
-            prod_wait(&ds_empty[ds_st], ((uint32_t)(j / kDsStages) & 1u) ^ 1u);
-            mbar_arrive_expect_tx(&ds_full[ds_st], 512);
-            bulk_load(smem + L::oDs + ds_st * 512, a.ds + ((int64_t)bh * n_qt + qt) * a.Np + j * 128, 512,
-                      &ds_full[ds_st]);
+      // ------------------------------------------------------------------ TMA producer: V.  Smoothing Q: the
+      // whole warp also turns each 512-byte ds row (ds[bh][qt][128 j .. 128 j + 128), the GEMV term of Alg1 L8,
+      // fetched kDsStages tiles ahead) into the B operand of the ds MMA: ds = hi + mid + lo, three exact tf32
+      // values (hi, mid: the top 11 significant bits of ds and of ds - hi; lo: the rest, <= 2 bits), so the
+      // tensor core adds ds to every row of S_j exactly up to its fp32 accumulation.
+      const float* ds_row = kSQ ? a.ds + ((int64_t)bh * n_qt + qt) * a.Np : nullptr;
+      auto fetch_ds = [&](int j) {
+        mbar_arrive_expect_tx(&ds_full[j % kDsStages], 512);
+        bulk_load(smem + L::oDs + (j % kDsStages) * 512, ds_row + j * 128, 512, &ds_full[j % kDsStages]);
+      };
+      if constexpr (kSQ) {
+        if (lane == 0)
+          for (int j = 0; j < nkv && j < kDsStages; ++j) fetch_ds(j);
+        __syncwarp();
+      }
+      for (int j = 0; j < nkv; ++j) {
+        if constexpr (kSQ) {
+          const int rs = j % kDsStages, os = j % kDsOps;
+          mbar_wait(&ds_full[rs], (uint32_t)(j / kDsStages) & 1u);
+          prod_wait(&dsop_empty[os], ((uint32_t)(j / kDsOps) & 1u) ^ 1u);
+          float4 g;
+          lds_f4(smem_u32(smem + L::oDs + rs * 512) + lane * 16, g);
+          const uint32_t dst = smem_u32(smem + L::oDsOp + os * 4096) + lane * 128;  // keys 4 lane .. 4 lane + 3
+          const float gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float hi = __uint_as_float(__float_as_uint(gv[t]) & 0xFFFFE000u);
+            const float r1 = gv[t] - hi;  // exact
+            const float mid = __uint_as_float(__float_as_uint(r1) & 0xFFFFE000u);
+            sts_v4(dst + 32 * t, __float_as_uint(hi), __float_as_uint(mid), __float_as_uint(r1 - mid), 0u);
           }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&dsop_full[os]);
+            if (j + kDsStages < nkv) fetch_ds(j + kDsStages);  // raw slot rs read by the whole warp
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
           const int st = j % kVStages;
           prod_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
@@ -308,8 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
                     &v_full[st]);
         }
+        __syncwarp();
       }
-      __syncwarp();
     } else if (warp == 1 || warp == 2) {
       // ------------------------------------------------------------------ MMA issuers: warp 1 issues the S
       // MMAs, warp 2 the PV MMAs (separate sub-partitions; disjoint scale-factor TMEM columns; each commits
@@ -342,6 +390,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t ad = make_smem_desc(smem_u32(sQ) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
             const uint64_t bd = make_smem_desc(smem_u32(sK) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
             mma(tbase + 128 * b, ad, bd, 128, ks, tbase + kColSFQ, tbase + kColSFK);
+          }
+          if constexpr (kSQ) {  // Alg1 L8: S_j += 1·ds_jᵀ (kind::tf32, K = 8: A rows [1,1,1,0, ..], B rows [hi,mid,lo,0, ..])
+            const int os = j % kDsOps;
+            mbar_wait(&dsop_full[os], (uint32_t)(j / kDsOps) & 1u);
+            tc_fence_after();
+            const uint64_t ad = make_smem_desc(smem_u32(smem + L::oDsOne), 16, 256, kLayoutSw32);
+            const uint64_t bd = make_smem_desc(smem_u32(smem + L::oDsOp + os * 4096), 16, 256, kLayoutSw32);
+            mma_tf32(tbase + 128 * b, ad, bd, make_idesc_tf32(128, 128), 1u);
+            mma_commit(&dsop_empty[os]);
           }
           mma_commit(&k_empty[st]);
           mma_commit(&s_full[b]);
@@ -432,40 +489,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       float bmax[8];
       auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
-        if constexpr (kSQ) {  // Alg1 L8: S += GEMV(q̄_i, K_j^T), the same 128-vector for every row (broadcast)
-          const uint32_t ds_s = smem_u32(smem + L::oDs + (j % kDsStages) * 512) + c * 128;
-#pragma unroll
-          for (int t = 0; t < 32; t += 4) {
-            float4 g;
-            lds_f4(ds_s + t * 4, g);
-            const f2 lo = fadd2(make_float2(f[t], f[t + 1]), make_float2(g.x, g.y));
-            const f2 hi = fadd2(make_float2(f[t + 2], f[t + 3]), make_float2(g.z, g.w));
-            f[t] = lo.x, f[t + 1] = lo.y, f[t + 2] = hi.x, f[t + 3] = hi.y;
-          }
-        }
         if constexpr (masked) {
 #pragma unroll
           for (int t = 0; t < 32; ++t) f[t] = (32 * c + t > lim) ? -INFINITY : f[t];
         }
-        if constexpr (masked || kSQ) tmem_st_32x32b_x32(s_addr + 32 * c, v);  // pass 2 reads the final S
+        if constexpr (masked) tmem_st_32x32b_x32(s_addr + 32 * c, v);  // pass 2 reads the final S
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
       };
-      if constexpr (kSQ) mbar_wait(&ds_full[j % kDsStages], (uint32_t)(j / kDsStages) & 1u);
-      if constexpr (kSQ) {  // two loads in flight (the ds chunk needs registers too)
-        uint32_t va[32], vb[32];
-#pragma unroll
-        for (int c = 0; c < 4; c += 2) {
-          tmem_ld_32x32b_x32(s_addr + 32 * c, va);
-          tmem_ld_32x32b_x32(s_addr + 32 * c + 32, vb);
-          tmem_ld_wait_regs(va);
-          tmem_ld_wait_regs(vb);
-          pass1(c, va);
-          pass1(c + 1, vb);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_empty[j % kDsStages]);  // ds slot read by this warp
-      } else {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
+      {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
         uint32_t va[32], vb[32], vc[32], vd[32];
         tmem_ld_32x32b_x32(s_addr, va);
         tmem_ld_32x32b_x32(s_addr + 32, vb);
@@ -500,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&m_full[slot]);  // per thread: orders its own slot write
       }
       const float nb = kDirect ? -eref * sl2 : kLog2_2688 - tmax * sl2;  // P̃2 (P̃) = 2^(S·sl2 + nb)
-      if constexpr (masked || kSQ) tmem_st_wait();
+      if constexpr (masked) tmem_st_wait();
       uint32_t va[32], vb[32];
       tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
       // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
@@ -767,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------------------------------- host
 template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
 cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D, kMX, kQSum>;
+  using L = Layout<D, kMX, kQSum, kSQ>;
   static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
@@ -791,7 +823,7 @@ cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
 
 template <int D, bool kSQ, bool kMX, bool kDirect, bool kQSum = false>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
-  if constexpr (!kSQ && !kDirect) {  // the north_star path: long sequences take the early-TMA instantiation
+  if constexpr (!kDirect) {  // the north_star path (and smoothing Q): long sequences take the early-TMA instantiation
     if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true, kQSum>(a, stream);
   }
   return launch_dk<D, kSQ, kMX, kDirect, false, kQSum>(a, stream);

@@ -213,7 +213,23 @@ __host__ __device__ constexpr uint32_t make_idesc_mxf4(uint32_t M, uint32_t N, u
   return make_idesc_nvf4(M, N) | (1u << 23) | ((2u * ks) << 29) | ((2u * ks) << 4);
 }
 
+// kind::tf32: D f32, A/B tf32 (format 2), K-major, K = 8 per instruction.
+__host__ __device__ constexpr uint32_t make_idesc_tf32(uint32_t M, uint32_t N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
 // ---------------------------------------------------------------- tcgen05: MMA / copy / commit
+// D[tmem] (+)= A[smem] x B[smem]^T, tf32 operands (the low 13 bits of each fp32 container are ignored).
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // D[tmem] (+)= A[smem] x B[smem]^T with per-16-element E4M3 scales SFA/SFB in TMEM.
 __device__ __forceinline__ void mma_nvf4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                          uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {

@@ -235,10 +235,11 @@ def test_paper_config_full_size_sampled(name):
 
 
 @pytest.mark.parametrize("causal", [False, True])
-@pytest.mark.parametrize("N,d", [(300, 64), (1000, 128), (128, 128)])
+@pytest.mark.parametrize("N,d", [(300, 64), (1000, 128), (128, 128), (15, 128), (1, 64), (2100, 128)])
 def test_attention_smooth_q_parity(N, d, causal):
     """Smoothing Q (Alg1 L5 + L8's GEMV, NEXT #1): the GPU path (q̄ tiles, Q - q̄ codes, ds = q̄·K_s^T in fp32,
-    S += ds in pass 1) against the oracle's fp64 Algorithm 1 with smoothing Q, north_star tolerance."""
+    S_j += 1·ds_jᵀ by a tf32 MMA on the hi/mid/lo split of ds) against the oracle's fp64 Algorithm 1 with
+    smoothing Q, element-wise.  N = 2100: 17 KV tiles, so the ds rings (4 raw, 3 operand slots) wrap."""
     B, H = 1, 2
     Q, K, V = synth.make_qkv(B, H, N, d, seed=11 * N + d, dtype=torch.bfloat16, device="cuda")
     Q = Q + 4.0 * torch.randn(1, H, 1, d, device="cuda", dtype=torch.float32).to(torch.bfloat16)  # shared offset
