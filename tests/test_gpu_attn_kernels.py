@@ -1,0 +1,19 @@
+"""Both attention kernels of the north_star path (attn.cu: two softmax warpgroups, the d = 128 default; attn3.cu:
+three softmax warpgroups, the d = 64 default) against the oracle, each forced for a whole process with
+SAGE3_ATTN_KERNEL, so the kernel that is not the default for a d is still parity-tested."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["2", "3"])
+def test_attention_kernel_selection_parity(kernel):
+    env = dict(os.environ, SAGE3_ATTN_KERNEL=kernel)
+    p = subprocess.run([sys.executable, os.path.join(HERE, "attn_kernel_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert p.returncode == 0 and "ALL OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]

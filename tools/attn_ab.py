@@ -2,6 +2,9 @@
 subprocess (SAGE3_LIB) and timed on the same inputs; the libraries alternate for `--reps` rounds.
 
     python tools/attn_ab.py build/lib_a.so build/lib_b.so [--shapes 32768:0,32768:1,1024:0] [--reps 2]
+
+A variant may also be `lib.so@VAR=VAL[,VAR=VAL]`: the same library run with extra environment variables
+(e.g. `paper_2505_11594_b200/libsage3.so@SAGE3_ATTN_KERNEL=3`).
 """
 import argparse
 import json
@@ -64,7 +67,9 @@ def main():
     res = {lib: [] for lib in a.libs}
     for _ in range(a.reps):
         for lib in a.libs:
-            env = dict(os.environ, SAGE3_LIB=os.path.abspath(lib))
+            path, _, extra = lib.partition("@")
+            env = dict(os.environ, SAGE3_LIB=os.path.abspath(path))
+            env.update(kv.split("=", 1) for kv in extra.split(",") if kv)
             p = subprocess.run([sys.executable, __file__, "--child", "--shapes", a.shapes, "--d", str(a.d),
                                 "--heads", str(a.heads), "--p-quant", a.p_quant], env=env, capture_output=True,
                                text=True, timeout=600)
