@@ -31,6 +31,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -59,6 +60,12 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_XCHG_TMEM
 #define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
 #endif
+#ifndef SAGE3_XFULL_WARP
+#define SAGE3_XFULL_WARP 0  // 1: one x_full arrival per softmax warp (after __syncwarp) instead of one per thread
+#endif
+#ifndef SAGE3_CORR_PV_FIRST
+#define SAGE3_CORR_PV_FIRST 0  // 1: the correction waits for PV_j before the (tmax, rowsum) exchange of tile j
+#endif
 #ifndef SAGE3_PROD_BACKOFF
 #define SAGE3_PROD_BACKOFF 0  // 1: TMA producers poll their empty barriers with test_wait + timed sleep
 #endif
@@ -69,6 +76,42 @@ __device__ __forceinline__ void prod_wait(uint64_t* bar, uint32_t parity) {
   ptx::mbar_wait(bar, parity);
 #endif
 }
+// ---- K/V tile sharing across a 2-CTA cluster (kMC): the two CTAs of a cluster are adjacent query tiles of one head
+// and read the same K̂/V̂ tiles, so each CTA TMA-loads half of every tile (K rows / V channels) with .multicast::cluster
+// into both CTAs' shared memory (CTA rank 0 also multicasts the tile's scale-factor atoms), and every ring slot is
+// released by both CTAs' MMA commits (multicast commit, "empty" barriers count 2).  Halves the L2 -> SM traffic and
+// the TMA issue of the K/V rings.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load_mc(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                             uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+
 // Which exp2 pairs of each 32-key chunk run on the FMA-pipe polynomial (bit i: pair i), per instantiation: the
 // share is 1/4 (two-level) or 5/16 (row-sum variant, whose softmax has no FADD2 row-sum tree); the positions were
 // picked by a same-box sweep of 12 masks (profiles/r2_poly_mask_sweep.txt; the spread is ±5% from ptxas scheduling).
@@ -164,7 +207,7 @@ struct Layout {
 // RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
 // of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
 // warpgroups are no longer independent in this mode.
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kMC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -211,11 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(q_full, 1);
     for (int s = 0; s < kKStages; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
+      mbar_init(&k_empty[s], kMC ? 2 : 1);
     }
     for (int s = 0; s < kVStages; ++s) {
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
+      mbar_init(&v_empty[s], kMC ? 2 : 1);
     }
     for (int b = 0; b < kSBufs; ++b) {
       mbar_init(&s_full[b], 1);
@@ -226,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[b], 4);  // one arrival per softmax warp
       mbar_init(&p_empty[b], 1);
     }
-    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 128);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], SAGE3_XFULL_WARP ? 4 : 128);
     for (int s = 0; s < kXSlots; ++s) mbar_init(&m_full[s], 128);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
@@ -280,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kMC) cluster_sync_all();  // both CTAs' barriers initialised before any multicast reaches them
   tc_fence_after();
   SAGE3_TRACE_EV(0, 127, 1);  // prologue done
   const uint32_t tbase = *tmem_slot;
@@ -302,9 +346,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row_k = bh * a.Np + j * 128;
           prod_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
-          tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
-          bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
-                    &k_full[st]);
+          if constexpr (kMC) {  // rows 64 r .. 64 r + 63 of the tile into both CTAs (tm_k has 64-row boxes here)
+            const uint32_t cr = cluster_ctarank();
+            tma_load_2d_mc(smem + L::oK + st * L::kKSlot + cr * 64 * L::kQKRow, &tm_k, &k_full[st], 0,
+                           row_k + 64 * (int)cr, 0x3);
+            if (cr == 0)
+              bulk_load_mc(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
+                           &k_full[st], 0x3);
+          } else {
+            tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
+            bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
+                      &k_full[st]);
+          }
         }
       }
       __syncwarp();
@@ -352,9 +405,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int st = j % kVStages;
           prod_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
-          tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
-          bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
-                    &v_full[st]);
+          if constexpr (kMC) {  // channels D/2 r .. of the Vᵀ tile into both CTAs (tm_v has D/2-row boxes here)
+            const uint32_t cr = cluster_ctarank();
+            tma_load_2d_mc(smem + L::oV + st * L::kVBytes + cr * (D / 2) * 64, &tm_v, &v_full[st], j * 64,
+                           bh * D + (D / 2) * (int)cr, 0x3);
+            if (cr == 0)
+              bulk_load_mc(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
+                           &v_full[st], 0x3);
+          } else {
+            tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
+            bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
+                      &v_full[st]);
+          }
         }
         __syncwarp();
       }
@@ -400,7 +462,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_tf32(tbase + 128 * b, ad, bd, make_idesc_tf32(128, 128), 1u);
             mma_commit(&dsop_empty[os]);
           }
-          mma_commit(&k_empty[st]);
+          if constexpr (kMC)
+            mma_commit_mc(&k_empty[st], 0x3);  // the slot is refilled by both CTAs' producers
+          else
+            mma_commit(&k_empty[st]);
           mma_commit(&s_full[b]);
           SAGE3_TRACE_EV(5, j, 3);
         };
@@ -436,7 +501,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                        tbase + kColSF1 + 4 * ks, ks > 0);
             }
           }
-          mma_commit(&v_empty[st]);
+          if constexpr (kMC)
+            mma_commit_mc(&v_empty[st], 0x3);
+          else
+            mma_commit(&v_empty[st]);
           mma_commit(&p_empty[pb]);
           mma_commit(&pv_full[b]);
           SAGE3_TRACE_EV(6, j, 3);
@@ -655,9 +723,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (tmax, rowsum) -> correction: every thread releases its own slot writes on x_full, so the hand-off is
       // ordered per thread (compute-sanitizer racecheck clean); P̂2 -> MMA: one arrival per warp after the
       // warp's proxy fences
+#if SAGE3_XFULL_WARP
+      __syncwarp();  // orders the warp's exchange-slot writes before lane 0's release
+      if (lane == 0) {
+        mbar_arrive(&x_full[slot]);
+        mbar_arrive(&p_full[pb]);
+      }
+#else
       mbar_arrive(&x_full[slot]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[pb]);
+#endif
 #endif
       SAGE3_TRACE_WARP(1 + par, j, 4);
     };
@@ -701,6 +777,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = __uint_as_float(xv[0]);
       const float rs2 = __uint_as_float(xv[1]);
 #else
+#if SAGE3_CORR_PV_FIRST
+      // PV_j first: its completion implies every softmax thread's x_full arrival (each precedes its warp's p_full
+      // arrival, which precedes the PV MMA), so the x_full wait below never sleeps.  (Waiting on x_full first
+      // sleeps through its 128 per-thread arrivals: ~75 wake-ups per tile per correction warp, ncu r2b.)
+      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
+#endif
       mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
       SAGE3_TRACE_EV(4, j, 1);
       const float tmax = lds_f32(xchg_s + slot * 1024);
@@ -720,7 +802,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!kQSum) l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
 #if !SAGE3_XCHG_TMEM
+#if !SAGE3_CORR_PV_FIRST
       mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
+#endif
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
 #endif
@@ -789,6 +873,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   SAGE3_TRACE_EV(4, 127, 2);  // correction: epilogue stores issued (thread 128)
   tc_fence_before();
   __syncthreads();
+  if constexpr (kMC) cluster_sync_all();  // the partner's multicasts and commits into this CTA have all landed
   SAGE3_TRACE_EV(0, 127, 3);  // all roles done
   if (warp == 2) {
     tc_fence_after();
@@ -821,8 +906,57 @@ cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// K/V tile sharing in 2-CTA clusters (kMC): non-causal north_star path, pairs of adjacent query tiles of one head.
+template <int D>
+cudaError_t launch_mc(const AttnArgs& a, cudaStream_t stream) {
+  using L = Layout<D, false, false, false>;
+  auto kern = attn_fwd_kernel<D, false, false, false, false, false, true>;
+  static std::atomic<bool> attr_done[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    if (e != cudaSuccess) return e;
+    attr_done[dev] = true;
+  }
+  const int BH = a.B * a.H;
+  CUtensorMap tq, tk, tv, to;
+  if (!make_map(&tq, a.q_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
+      !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 64) ||  // half K tiles
+      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D / 2) ||  // half Vᵀ tiles
+      !make_map_o(&to, a.o, a.o_dtype, a.B, a.H, a.N, D, a.o_sb, a.o_sh, a.o_sn))
+    return cudaErrorInvalidValue;
+  const int64_t units = a.unit_end - a.unit_begin;
+  if (units <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)units, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = L::kSmemAlloc;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, a);
+}
+bool kv_multicast_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SAGE3_KV_MULTICAST");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int D, bool kSQ, bool kMX, bool kDirect, bool kQSum = false>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
+  if constexpr (!kSQ && !kMX && !kDirect && !kQSum) {
+    if (kv_multicast_enabled() && !a.causal && (a.Np / 128) % 2 == 0 && a.unit_begin % 2 == 0 &&
+        (a.unit_end - a.unit_begin) % 2 == 0)
+      return launch_mc<D>(a, stream);
+  }
   if constexpr (!kDirect) {  // the north_star path (and smoothing Q): long sequences take the early-TMA instantiation
     if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true, kQSum>(a, stream);
   }
