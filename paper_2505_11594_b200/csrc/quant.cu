@@ -553,7 +553,8 @@ template <typename T, int D>
 __global__ void __launch_bounds__(256) smooth_q_ds_kernel(QKArgs qa) {
   extern __shared__ __align__(16) float dsm_f[];
   float* kst = dsm_f;            // [D][128] smoothed K of this key chunk, transposed
-  float* qmt = dsm_f + D * 128;  // [D][64] q̄ of 64 query tiles, transposed
+  constexpr int kQS = 68;        // row stride of the transposed q̄ block (16-byte rows, 4-way store conflicts)
+  float* qmt = dsm_f + D * 128;  // [D][kQS] q̄ of 64 query tiles, transposed
   const int chunk = blockIdx.x, bh = blockIdx.y;
   const int b = bh / qa.H, h = bh % qa.H;
   const int t = threadIdx.x, nt = qa.Np >> 7;
@@ -575,20 +576,34 @@ __global__ void __launch_bounds__(256) smooth_q_ds_kernel(QKArgs qa) {
     for (int e = 0; e < 8; ++e) kst[(c8 * 8 + e) * 128 + key] = x[e];
   }
   const int kg = t & 31, ig = t >> 5;
+  // q̄ blocks of 64 tiles: coalesced global reads (channels fastest across threads) into registers one block ahead,
+  // stored transposed once the previous block has been consumed
+  constexpr int kPre = 64 * D / 256;
+  float pre[kPre];
+  auto fetch = [&](int i0) {
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+      const int i = t + 256 * k, ti = i / D, c = i % D;
+      pre[k] = i0 + ti < nt ? qa.q_mean[((int64_t)bh * nt + i0 + ti) * D + c] : 0.0f;
+    }
+  };
+  fetch(0);
   for (int i0 = 0; i0 < nt; i0 += 64) {
     __syncthreads();  // kst written / previous block's qmt consumed
-    for (int i = t; i < 64 * D; i += 256) {  // tiles fastest across threads (conflict-free transposed store)
-      const int ti = i % 64, c = i / 64;
-      qmt[c * 64 + ti] = i0 + ti < nt ? qa.q_mean[((int64_t)bh * nt + i0 + ti) * D + c] : 0.0f;
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+      const int i = t + 256 * k, ti = i / D, c = i % D;
+      qmt[c * kQS + ti] = pre[k];
     }
+    if (i0 + 64 < nt) fetch(i0 + 64);
     __syncthreads();
     f2 acc[8][2];
 #pragma unroll
     for (int ii = 0; ii < 8; ++ii) acc[ii][0] = acc[ii][1] = make_float2(0.f, 0.f);
 #pragma unroll 4
     for (int c = 0; c < D; ++c) {
-      const float4 a0 = reinterpret_cast<const float4*>(qmt + c * 64 + ig * 8)[0];
-      const float4 a1 = reinterpret_cast<const float4*>(qmt + c * 64 + ig * 8)[1];
+      const float4 a0 = reinterpret_cast<const float4*>(qmt + c * kQS + ig * 8)[0];
+      const float4 a1 = reinterpret_cast<const float4*>(qmt + c * kQS + ig * 8)[1];
       const float4 bb = reinterpret_cast<const float4*>(kst + c * 128)[kg];
       const f2 b01 = make_float2(bb.x, bb.y), b23 = make_float2(bb.z, bb.w);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
@@ -676,7 +691,7 @@ cudaError_t launch_t(const QKArgs& qk, const VArgs& v, double* ws, cudaStream_t 
   }
   if (qk.q_mean) {  // smoothing Q: the GEMV term, after every q̄ of the head is written
     static bool ds_attr[64] = {};
-    constexpr int kDsSmem = (D * 128 + D * 64) * 4;
+    constexpr int kDsSmem = (D * 128 + D * 68) * 4;
     if (dev < 64 && !ds_attr[dev]) {
       cudaError_t e = cudaFuncSetAttribute(smooth_q_ds_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDsSmem);
       if (e != cudaSuccess) return e;
