@@ -595,15 +595,17 @@ cudaError_t launch3(const AttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
-// The north_star path (NVFP4, paper-exact two-level P, no smoothing Q) takes this kernel for d = 64, where it measured
-// faster than attn.cu (C3-shaped 768 vs 718 TOPS; d = 128: 1485 vs 1494 at N = 32K).  SAGE3_ATTN_KERNEL=2 / =3 force
-// attn.cu / this kernel for every d (experiments, A/B runs).
-bool attention3_enabled(int d) {
+// The north_star path (NVFP4, paper-exact two-level P, no smoothing Q) takes this kernel for d = 64 when it measured
+// faster than attn.cu (same-box A/B, B=1, H=32, TOPS attn.cu / attn3.cu: non-causal N = 1K 378 / 349, 2K 508 / 475,
+// 4K 652 / 649, 8K 695 / 722, 16K 711 / 763; causal 2K 316 / 332, 8K 550 / 620, 32K 670 / 767; C3-shaped 718 / 768):
+// causal, or N >= 8K.  d = 128 stays on attn.cu (1494 vs 1485 at N = 32K).  SAGE3_ATTN_KERNEL=2 / =3 force attn.cu /
+// this kernel for every shape (experiments, A/B runs).
+bool attention3_enabled(int d, int N, int causal) {
   static const int force = [] {
     const char* e = std::getenv("SAGE3_ATTN_KERNEL");
     return e == nullptr ? 0 : e[0] == '2' ? 2 : e[0] == '3' ? 3 : 0;
   }();
-  return force == 3 || (force == 0 && d == 64);
+  return force == 3 || (force == 0 && d == 64 && (causal || N >= 8192));
 }
 
 cudaError_t launch_attention3(const AttnArgs& a, cudaStream_t stream) {

@@ -111,7 +111,7 @@ struct AttnArgs {
 // Returns cudaSuccess or the launch / driver error.  `drv_err` receives a CUresult on descriptor failure.
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream);
 // attn3.cu: the north_star path (NVFP4, two-level P, no smoothing Q) with three softmax warpgroups per CTA.
-bool attention3_enabled(int d);
+bool attention3_enabled(int d, int N, int causal);
 cudaError_t launch_attention3(const AttnArgs& a, cudaStream_t stream);
 // The NEXT #2 lazy-reference variant (attn_lazy.cu; p_quant = SAGE3_P_TWO_LEVEL_LAZY, no smoothing Q).
 cudaError_t launch_attention_lazy(const AttnArgs& a, cudaStream_t stream);
