@@ -1,29 +1,10 @@
-// attn.cu — sm_100a SageAttention3 FP4 attention forward: Algorithm 1 L6-L13.
-//
-// One CTA = one 128-row query tile Q_i of one (b,h); loop over 128-key tiles j (B_q = B_kv = 128).
-// Warp roles (16 warps, 4 warpgroups, 1 CTA per SM):
-//   WG0 warp 0   TMA producer of Q̂_i + s_Q (once) and K̂_j + s_K (kKStages ring)
-//       warp 3   TMA producer of V̂ᵀ_j + s_V (kVStages ring)
-//       warp 1   MMA issuer (one elected lane):
-//                  S_j  = FP4MM(Q̂_i, s_Q, K̂_j, s_K)      tcgen05.mma kind::mxf4nvf4, M=128 N=128 K=d
-//                  PV_j = FP4MM(P̂2_j, s_P2, V̂_j, s_V)    M=128 N=d K=128, written over S_j's TMEM columns
-//                scale factors go smem -> TMEM with tcgen05.cp.32x128b.warpx4, in MMA issue order
-//       warp 2   TMEM allocator (512 columns)
-//   WG2, WG3     softmax + two-level P quantization, one query row per thread (TMEM lane = row);
-//                WG2 takes the even KV tiles, WG3 the odd ones.  A tile's P̂2
-//                codes and s_P2 depend only on that tile's row max (see below), so the two warpgroups
-//                never synchronise with each other.
-//   WG1          correction: owns the online-softmax recurrence (m, l; Alg1 L9) and O in registers:
-//                O = α·O + s_P1·PV_j (Alg1 L11), then O/l (L13) and the store.
-//
-// Two-level P in tile-local form (reading c14): with tmax_j = rowmax(S_ij),
-// m_j = max(m_{j-1}, tmax_j) and the scale folded into log2 units (sl2 = scale·log2 e):
-//     P̃2_j = P̃_j / s_P1 = 2688 · 2^{sl2 (S − tmax_j)}         (max element = 2688 -> s_P2 = 448, code 6)
-//     s_P1 = rowmax(P̃_j)/2688 = 2^{sl2 (tmax_j − m_j)} / 2688
-//     l_j  = 2^{sl2 (m_{j-1} − m_j)} l_{j-1} + s_P1 · rowsum(P̃2_j)
-// The 16-key block maxima of S are taken once (pass 1) and reused twice (the paper's "reuse" of the
-// block max): their max is tmax_j, and 2688·2^{sl2 (bmax − tmax)} is the block amax of P̃2
-// that sets s_P2 (exp is monotone, and the argmax element is computed by the identical instruction).
+// attn_persist.cu — the attention kernel of attn.cu as of commit 6bc171b with its persistent instantiation, used for
+// short sequences (N <= SAGE3_PERSIST_MAX_N) on the north_star path: grid = min(units, SMs) and each CTA walks units
+// b, b + gridDim, ..., every role indexing its rings and TMEM buffers by the CTA's running KV-tile count, so a unit's
+// prologue (Q̂ and the first K̂/V̂ tiles, the first S MMAs) overlaps its predecessor's last tiles and epilogue (second
+// Q̂ slot, dedicated O staging buffer).  Kept in its own translation unit: folding it into attn.cu moved ptxas code
+// generation of the long-sequence instantiation (-3.5% at N = 32K).
+// Algorithm 1 L6-L13, tile-local two-level P (reading c14), identical arithmetic.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -60,12 +41,6 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_XCHG_TMEM
 #define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
 #endif
-#ifndef SAGE3_XFULL_WARP
-#define SAGE3_XFULL_WARP 0  // 1: one x_full arrival per softmax warp (after __syncwarp) instead of one per thread
-#endif
-#ifndef SAGE3_CORR_PV_FIRST
-#define SAGE3_CORR_PV_FIRST 0  // 1: the correction waits for PV_j before the (tmax, rowsum) exchange of tile j
-#endif
 #ifndef SAGE3_PROD_BACKOFF
 #define SAGE3_PROD_BACKOFF 0  // 1: TMA producers poll their empty barriers with test_wait + timed sleep
 #endif
@@ -76,42 +51,6 @@ __device__ __forceinline__ void prod_wait(uint64_t* bar, uint32_t parity) {
   ptx::mbar_wait(bar, parity);
 #endif
 }
-// ---- K/V tile sharing across a 2-CTA cluster (kMC): the two CTAs of a cluster are adjacent query tiles of one head
-// and read the same K̂/V̂ tiles, so each CTA TMA-loads half of every tile (K rows / V channels) with .multicast::cluster
-// into both CTAs' shared memory (CTA rank 0 also multicasts the tile's scale-factor atoms), and every ring slot is
-// released by both CTAs' MMA commits (multicast commit, "empty" barriers count 2).  Halves the L2 -> SM traffic and
-// the TMA issue of the K/V rings.
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1,
-                                               uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
-      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_load_mc(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
-                                             uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   smem_u32(bar)),
-               "h"(mask)
-               : "memory");
-}
-
 // Which exp2 pairs of each 32-key chunk run on the FMA-pipe polynomial (bit i: pair i), per instantiation: the
 // share is 1/4 (two-level) or 5/16 (row-sum variant, whose softmax has no FADD2 row-sum tree); the positions were
 // picked by a same-box sweep of 12 masks (profiles/r2_poly_mask_sweep.txt; the spread is ±5% from ptxas scheduling).
@@ -127,7 +66,6 @@ constexpr int kKStages = 5, kVStages = 4;
 constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
 constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
 constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
-constexpr int kDsOps = 3;     // smoothing Q: tf32 B operands of the ds MMA (tile j -> j % 3)
 constexpr int kThreads = 512;
 // Per-thread register budgets after setmaxnreg (one warp of each warpgroup per SM sub-partition:
 // kRegWG0 + 2 kRegSoftmax + kRegCorrection = 512 = 64K registers / 128 lanes).
@@ -162,7 +100,7 @@ constexpr int kSBufs = 3;
 // TMEM columns per S/PV buffer (tile j -> kColRS + 16 (j % 3)); the ones operand's scale factors sit at kColSF1.
 constexpr uint32_t kColSF1 = 432, kColRS = 448;
 
-template <int D, bool kMX, bool kQSum = false, bool kSQ = false>
+template <int D, bool kMX, bool kQSum = false, bool kPersist = false>
 struct Layout {
   static constexpr int kQKRow = D / 2;          // bytes per Q/K row (64 or 32)
   static constexpr int kQBytes = 128 * kQKRow;   // Q tile codes
@@ -188,13 +126,15 @@ struct Layout {
   // kQSum: the all-ones B operand (16 rows x 128 keys, E2M1 1.0 = code 2 in every nibble) and its SF atoms (E4M3 1.0)
   static constexpr int oOnes = ((oDs + kDsStages * 512 + 1023) / 1024) * 1024;
   static constexpr int oOnesSF = oOnes + 1024;
-  // kSQ: the tf32 operands of the ds MMA (S += 1·dsᵀ): A = 128 identical rows [1,1,1,0, 1,1,1,0] (4 KB), and
-  // kDsOps B slots of 128 keys x 8 tf32 (32 B per key: [hi, mid, lo, 0] of ds in one 16-byte half, zeros in the other)
-  static constexpr int oDsOne = oOnes;
-  static constexpr int oDsOp = oDsOne + 4096;
-  static constexpr int oBar = kQSum ? oOnesSF + 1024 : kSQ ? oDsOp + kDsOps * 4096 : oDs + kDsStages * 512;
+  static constexpr int oEnd0 = kQSum ? oOnesSF + 1024 : oDs + kDsStages * 512;
+  // kPersist: a second Q slot (the next unit's Q̂ loads while the current unit runs) and a dedicated O staging
+  // buffer (the K/V rings are busy with the next unit when an epilogue runs), fp32-sized
+  static constexpr int oQ1 = ((oEnd0 + 1023) / 1024) * 1024;
+  static constexpr int oQSF1 = oQ1 + ((kQBytes + 1023) / 1024) * 1024;
+  static constexpr int oStage = ((oQSF1 + kQKSF + 1023) / 1024) * 1024;
+  static constexpr int oBar = kPersist ? oStage + D * 128 * 4 : oEnd0;
   static constexpr int kNumBars =
-      1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages + 2 * kDsOps;
+      4 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages;
   static constexpr int oTmem = oBar + kNumBars * 8;
   static constexpr int kBytes = oTmem + 16;
   static constexpr int kSmemAlloc = kBytes + 1024;  // slack for manual 1024-B alignment
@@ -207,22 +147,21 @@ struct Layout {
 // RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
 // of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
 // warpgroups are no longer independent in this mode.
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kMC = false>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kPersist>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                     const AttnArgs a) {
-  using L = Layout<D, kMX, kQSum, kSQ>;
+  using L = Layout<D, kMX, kQSum, kPersist>;
   extern __shared__ uint8_t smem_raw[];
   // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
   __shared__ __align__(1024) float2 s_lut[128];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
-  uint8_t* sQ = smem + L::oQ;
-  uint8_t* sQSF = smem + L::oQSF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = q_full + 1;
+  uint64_t* q_full = bars;       // [2]: Q̂ slot loaded (kPersist: unit ui uses slot ui % 2)
+  uint64_t* q_empty = bars + 2;  // [2]: kPersist: the S MMAs of the slot's unit are done with it
+  uint64_t* k_full = bars + 4;
   uint64_t* k_empty = k_full + kKStages;
   uint64_t* v_full = k_empty + kKStages;
   uint64_t* v_empty = v_full + kVStages;
@@ -232,33 +171,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = b_empty + kSBufs;    // softmax -> MMA: P̂2_j / s_P2 in smem buffer j%4, S_j consumed
   uint64_t* p_empty = p_full + kPBufs;    // MMA -> softmax: PV_j done with smem buffer j%4
   uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8 (smem mode)
-  uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (bulk copy)
-  uint64_t* ds_empty = ds_full + kDsStages;  // (unused)
+  uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (TMA)
+  uint64_t* ds_empty = ds_full + kDsStages;  // softmax -> V producer: slot read
   uint64_t* m_full = ds_empty + kDsStages;    // direct P: m_j of tile j in xchg slot j%8 (softmax -> softmax)
-  uint64_t* dsop_full = m_full + kXSlots;     // smoothing Q: V-producer warp -> MMA: tf32 ds operand of tile j in slot j%3
-  uint64_t* dsop_empty = dsop_full + kDsOps;  // MMA -> V-producer warp: the ds MMA of tile j read slot j%3
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::oTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Work unit u = unit_begin + blockIdx.x of the flattened (b·h, q-tile) space, q tiles fastest and in
   // descending order within a head (CTAs of one head run together and share K/V in L2; longest first under
   // causal masking).  sage3_attn_fwd covers every unit; the multi-GPU launcher gives each rank a range.
+  // kPersist (short sequences): grid = min(units, SMs) and CTA b processes units b, b + gridDim, ... one after the
+  // other; every role walks the same unit sequence and indexes its rings and TMEM buffers by the CTA's running KV
+  // tile count g (= g0 of the unit + j), so the pipelines run across unit boundaries (the next unit's Q̂ and first
+  // K/V tiles load while the current unit's epilogue runs).
   const int n_qt = a.Np >> 7;
-  const int64_t unit = a.unit_begin + (int64_t)blockIdx.x;
-  const int bh = (int)(unit / n_qt);
-  const int qt = n_qt - 1 - (int)(unit % n_qt);
-  const int nkv = a.causal ? qt + 1 : n_qt;
+  const int64_t n_units = a.unit_end - a.unit_begin;
+  int bh = 0, qt = 0, nkv = 0;
+  auto unit_of = [&](int ui) {  // (bh, qt, nkv) of this CTA's unit ui; false past the last one
+    const int64_t u = (int64_t)blockIdx.x + (int64_t)ui * gridDim.x;
+    if ((!kPersist && ui > 0) || u >= n_units) return false;
+    const int64_t unit = a.unit_begin + u;
+    bh = (int)(unit / n_qt);
+    qt = n_qt - 1 - (int)(unit % n_qt);
+    nkv = a.causal ? qt + 1 : n_qt;
+    return true;
+  };
+  unit_of(0);
+  auto q_slot = [&](int ui) { return kPersist ? (ui & 1) : 0; };
+  auto sQ_of = [&](int qs) { return smem + (qs ? L::oQ1 : L::oQ); };
+  auto sQSF_of = [&](int qs) { return smem + (qs ? L::oQSF1 : L::oQSF); };
 
   SAGE3_TRACE_EV(0, 127, 0);  // CTA start (thread 0)
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
     for (int s = 0; s < kKStages; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], kMC ? 2 : 1);
+      mbar_init(&k_empty[s], 1);
     }
     for (int s = 0; s < kVStages; ++s) {
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], kMC ? 2 : 1);
+      mbar_init(&v_empty[s], 1);
     }
     for (int b = 0; b < kSBufs; ++b) {
       mbar_init(&s_full[b], 1);
@@ -269,15 +224,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[b], 4);  // one arrival per softmax warp
       mbar_init(&p_empty[b], 1);
     }
-    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], SAGE3_XFULL_WARP ? 4 : 128);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 128);
     for (int s = 0; s < kXSlots; ++s) mbar_init(&m_full[s], 128);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
-      mbar_init(&ds_empty[s], 1);
-    }
-    for (int s = 0; s < kDsOps; ++s) {
-      mbar_init(&dsop_full[s], 1);
-      mbar_init(&dsop_empty[s], 1);
+      mbar_init(&ds_empty[s], 4);  // one arrival per softmax warp of the tile's warpgroup
     }
     fence_mbar_init();
     prefetch_tmap(&tm_q);
@@ -289,9 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // while the same code path costs 2-4% at N = 1K).
     if constexpr (kEarly) {
     const int row_q = bh * a.Np + qt * 128;
-    mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
-    tma_load_2d(smem + L::oQ, &tm_q, q_full, 0, row_q);
-    bulk_load(smem + L::oQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
+    mbar_arrive_expect_tx(&q_full[0], L::kQBytes + L::kQKSF);
+    tma_load_2d(smem + L::oQ, &tm_q, &q_full[0], 0, row_q);
+    bulk_load(smem + L::oQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, &q_full[0]);
     for (int j = 0; j < nkv && j < SAGE3_EARLY_K; ++j) {
       const int row_k = bh * a.Np + j * 128;
       mbar_arrive_expect_tx(&k_full[j], L::kKBytes + L::kQKSF);
@@ -314,16 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = threadIdx.x; i < 512; i += kThreads) ones[i] = i < 256 ? 0x22222222u : 0x38383838u;
     fence_proxy_async_smem();
   }
-  if constexpr (kSQ) {  // the ds MMA's constant A operand (rows [1,1,1,0, 1,1,1,0]) and zeroed B slots
-    uint32_t* one = reinterpret_cast<uint32_t*>(smem + L::oDsOne);
-    for (int i = threadIdx.x; i < 1024; i += kThreads) one[i] = (i & 3) == 3 ? 0u : 0x3F800000u;
-    uint32_t* op = reinterpret_cast<uint32_t*>(smem + L::oDsOp);
-    for (int i = threadIdx.x; i < kDsOps * 1024; i += kThreads) op[i] = 0u;
-    fence_proxy_async_smem();
-  }
   tc_fence_before();
   __syncthreads();
-  if constexpr (kMC) cluster_sync_all();  // both CTAs' barriers initialised before any multicast reaches them
   tc_fence_after();
   SAGE3_TRACE_EV(0, 127, 1);  // prologue done
   const uint32_t tbase = *tmem_slot;
@@ -334,26 +277,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer: Q, K
       if (elect_one()) {
-        constexpr bool early = kEarly;  // Q and K 0.. already requested in the prologue
-        if (!early) {
-          const int row_q = bh * a.Np + qt * 128;
-          mbar_arrive_expect_tx(q_full, L::kQBytes + L::kQKSF);
-          tma_load_2d(sQ, &tm_q, q_full, 0, row_q);
-          bulk_load(sQSF, a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, q_full);
-        }
-        for (int j = early ? SAGE3_EARLY_K : 0; j < nkv; ++j) {
-          const int st = j % kKStages;
-          const int row_k = bh * a.Np + j * 128;
-          prod_wait(&k_empty[st], ((uint32_t)(j / kKStages) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
-          if constexpr (kMC) {  // rows 64 r .. 64 r + 63 of the tile into both CTAs (tm_k has 64-row boxes here)
-            const uint32_t cr = cluster_ctarank();
-            tma_load_2d_mc(smem + L::oK + st * L::kKSlot + cr * 64 * L::kQKRow, &tm_k, &k_full[st], 0,
-                           row_k + 64 * (int)cr, 0x3);
-            if (cr == 0)
-              bulk_load_mc(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
-                           &k_full[st], 0x3);
-          } else {
+        for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
+          const bool early = kEarly && ui == 0;  // Q and K 0.. already requested in the prologue
+          const int qs = q_slot(ui);
+          if (!early) {
+            if (kPersist && ui >= 2) prod_wait(&q_empty[qs], ((uint32_t)((ui >> 1) - 1) & 1u));
+            const int row_q = bh * a.Np + qt * 128;
+            mbar_arrive_expect_tx(&q_full[qs], L::kQBytes + L::kQKSF);
+            tma_load_2d(sQ_of(qs), &tm_q, &q_full[qs], 0, row_q);
+            bulk_load(sQSF_of(qs), a.q_sf + (int64_t)(row_q >> 7) * L::kQKSF, L::kQKSF, &q_full[qs]);
+          }
+          for (int j = early ? SAGE3_EARLY_K : 0; j < nkv; ++j) {
+            const int g = g0 + j, st = g % kKStages;
+            const int row_k = bh * a.Np + j * 128;
+            prod_wait(&k_empty[st], ((uint32_t)(g / kKStages) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&k_full[st], L::kKBytes + L::kQKSF);
             tma_load_2d(smem + L::oK + st * L::kKSlot, &tm_k, &k_full[st], 0, row_k);
             bulk_load(smem + L::oKSF + st * L::kQKSF, a.k_sf + (int64_t)(row_k >> 7) * L::kQKSF, L::kQKSF,
                       &k_full[st]);
@@ -362,64 +300,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     } else if (warp == 3) {
-      // ------------------------------------------------------------------ TMA producer: V.  Smoothing Q: the
-      // whole warp also turns each 512-byte ds row (ds[bh][qt][128 j .. 128 j + 128), the GEMV term of Alg1 L8,
-      // fetched kDsStages tiles ahead) into the B operand of the ds MMA: ds = hi + mid + lo, three exact tf32
-      // values (hi, mid: the top 11 significant bits of ds and of ds - hi; lo: the rest, <= 2 bits), so the
-      // tensor core adds ds to every row of S_j exactly up to its fp32 accumulation.
-      const float* ds_row = kSQ ? a.ds + ((int64_t)bh * n_qt + qt) * a.Np : nullptr;
-      auto fetch_ds = [&](int j) {
-        mbar_arrive_expect_tx(&ds_full[j % kDsStages], 512);
-        bulk_load(smem + L::oDs + (j % kDsStages) * 512, ds_row + j * 128, 512, &ds_full[j % kDsStages]);
-      };
-      if constexpr (kSQ) {
-        if (lane == 0)
-          for (int j = 0; j < nkv && j < kDsStages; ++j) fetch_ds(j);
-        __syncwarp();
-      }
-      for (int j = 0; j < nkv; ++j) {
-        if constexpr (kSQ) {
-          const int rs = j % kDsStages, os = j % kDsOps;
-          mbar_wait(&ds_full[rs], (uint32_t)(j / kDsStages) & 1u);
-          prod_wait(&dsop_empty[os], ((uint32_t)(j / kDsOps) & 1u) ^ 1u);
-          float4 g;
-          lds_f4(smem_u32(smem + L::oDs + rs * 512) + lane * 16, g);
-          const uint32_t dst = smem_u32(smem + L::oDsOp + os * 4096) + lane * 128;  // keys 4 lane .. 4 lane + 3
-          const float gv[4] = {g.x, g.y, g.z, g.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float hi = __uint_as_float(__float_as_uint(gv[t]) & 0xFFFFE000u);
-            const float r1 = gv[t] - hi;  // exact
-            const float mid = __uint_as_float(__float_as_uint(r1) & 0xFFFFE000u);
-            sts_v4(dst + 32 * t, __float_as_uint(hi), __float_as_uint(mid), __float_as_uint(r1 - mid), 0u);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&dsop_full[os]);
-            if (j + kDsStages < nkv) fetch_ds(j + kDsStages);  // raw slot rs read by the whole warp
-          }
-          __syncwarp();
-        }
-        if (elect_one()) {
-          const int st = j % kVStages;
-          prod_wait(&v_empty[st], ((uint32_t)(j / kVStages) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
-          if constexpr (kMC) {  // channels D/2 r .. of the Vᵀ tile into both CTAs (tm_v has D/2-row boxes here)
-            const uint32_t cr = cluster_ctarank();
-            tma_load_2d_mc(smem + L::oV + st * L::kVBytes + cr * (D / 2) * 64, &tm_v, &v_full[st], j * 64,
-                           bh * D + (D / 2) * (int)cr, 0x3);
-            if (cr == 0)
-              bulk_load_mc(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
-                           &v_full[st], 0x3);
-          } else {
+      // ------------------------------------------------------------------ TMA producer: V
+      if (elect_one()) {
+        for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
+          for (int j = 0; j < nkv; ++j) {
+            const int g = g0 + j;
+            if constexpr (kSQ) {  // ds[bh][qt][128 j .. 128 j + 128): the GEMV term of this (query, key) tile
+              const int ds_st = g % kDsStages;
+              prod_wait(&ds_empty[ds_st], ((uint32_t)(g / kDsStages) & 1u) ^ 1u);
+              mbar_arrive_expect_tx(&ds_full[ds_st], 512);
+              bulk_load(smem + L::oDs + ds_st * 512, a.ds + ((int64_t)bh * n_qt + qt) * a.Np + j * 128, 512,
+                        &ds_full[ds_st]);
+            }
+            const int st = g % kVStages;
+            prod_wait(&v_empty[st], ((uint32_t)(g / kVStages) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&v_full[st], L::kVBytes + L::kVSF);
             tma_load_2d(smem + L::oV + st * L::kVBytes, &tm_v, &v_full[st], j * 64, bh * D);
             bulk_load(smem + L::oVSF + st * L::kVSF, a.v_sf + ((int64_t)bh * n_qt + j) * L::kVSF, L::kVSF,
                       &v_full[st]);
           }
         }
-        __syncwarp();
       }
+      __syncwarp();
     } else if (warp == 1 || warp == 2) {
       // ------------------------------------------------------------------ MMA issuers: warp 1 issues the S
       // MMAs, warp 2 the PV MMAs (separate sub-partitions; disjoint scale-factor TMEM columns; each commits
@@ -435,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             mma_nvf4(d, ad, bd, make_idesc_nvf4(128, n), sfa + 4 * ks, sfb + 4 * ks, ks > 0);
         };
-        auto issue_s = [&](int j) {
+        auto issue_s = [&](int j, const uint8_t* sQ) {  // j: the CTA's running tile count g
           const int b = j % kSBufs, st = j % kKStages;
           SAGE3_TRACE_EV(5, j, 0);
           mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
@@ -453,19 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = make_smem_desc(smem_u32(sK) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
             mma(tbase + 128 * b, ad, bd, 128, ks, tbase + kColSFQ, tbase + kColSFK);
           }
-          if constexpr (kSQ) {  // Alg1 L8: S_j += 1·ds_jᵀ (kind::tf32, K = 8: A rows [1,1,1,0, ..], B rows [hi,mid,lo,0, ..])
-            const int os = j % kDsOps;
-            mbar_wait(&dsop_full[os], (uint32_t)(j / kDsOps) & 1u);
-            tc_fence_after();
-            const uint64_t ad = make_smem_desc(smem_u32(smem + L::oDsOne), 16, 256, kLayoutSw32);
-            const uint64_t bd = make_smem_desc(smem_u32(smem + L::oDsOp + os * 4096), 16, 256, kLayoutSw32);
-            mma_tf32(tbase + 128 * b, ad, bd, make_idesc_tf32(128, 128), 1u);
-            mma_commit(&dsop_empty[os]);
-          }
-          if constexpr (kMC)
-            mma_commit_mc(&k_empty[st], 0x3);  // the slot is refilled by both CTAs' producers
-          else
-            mma_commit(&k_empty[st]);
+          mma_commit(&k_empty[st]);
           mma_commit(&s_full[b]);
           SAGE3_TRACE_EV(5, j, 3);
         };
@@ -501,27 +391,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                        tbase + kColSF1 + 4 * ks, ks > 0);
             }
           }
-          if constexpr (kMC)
-            mma_commit_mc(&v_empty[st], 0x3);
-          else
-            mma_commit(&v_empty[st]);
+          mma_commit(&v_empty[st]);
           mma_commit(&p_empty[pb]);
           mma_commit(&pv_full[b]);
           SAGE3_TRACE_EV(6, j, 3);
         };
         if (warp == 1) {
-          mbar_wait(q_full, 0);
-          tc_fence_after();
+          for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
+            const int qs = q_slot(ui);
+            mbar_wait(&q_full[qs], kPersist ? (uint32_t)((ui >> 1) & 1) : 0u);
+            tc_fence_after();
 #pragma unroll
-          for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * at, sf_desc(sQSF + 512 * at));
-          for (int j = 0; j < nkv; ++j) issue_s(j);  // S_j into buffer j%3 once the correction freed it
+            for (int at = 0; at < kQKAtoms; ++at)
+              tmem_cp_32x128b_x4(tbase + kColSFQ + 4 * at, sf_desc(sQSF_of(qs) + 512 * at));
+            for (int j = 0; j < nkv; ++j) issue_s(g0 + j, sQ_of(qs));  // S into buffer g%3 once it is free
+            if constexpr (kPersist) mma_commit(&q_empty[qs]);      // the slot's S MMAs are issued: reusable
+          }
         } else {
           if constexpr (kQSum) {
 #pragma unroll
             for (int at = 0; at < 2; ++at)
               tmem_cp_32x128b_x4(tbase + kColSF1 + 4 * at, sf_desc(smem + L::oOnesSF + 512 * at));
           }
-          for (int j = 0; j < nkv; ++j) issue_pv(j);
+          for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui)
+            for (int j = 0; j < nkv; ++j) issue_pv(g0 + j);
         }
       }
       __syncwarp();
@@ -529,9 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (wg >= 2) {
     // -------------------------------------------------------------------- softmax + two-level P quant
     setmaxnreg_inc<reg_softmax<D>()>();
-    const int par = wg - 2;                 // this warpgroup's KV-tile parity
+    const int par = wg - 2;                 // this warpgroup's KV-tile parity (of the running tile count g)
     const int r = threadIdx.x - 128 * wg;   // query row in the tile == TMEM lane
-    const int q_row = qt * 128 + r;
+    int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = a.scale * kLog2e;
     const f2 sl2x2 = make_float2(sl2, sl2);
@@ -539,14 +432,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // One KV tile (Alg1 L8-L10 for this warpgroup's rows).  Only the last tile can need masking (keys >= N,
     // or the causal diagonal), so it is a separate instantiation outside the hot loop: the loop body is
     // straight-line code with no masking branches (instruction-cache friendly).
-    auto tile = [&](const int j, auto masked_tag) {
+    auto tile = [&](const int j, const int g, auto masked_tag) {  // j: KV tile of the unit, g: running count
       constexpr bool masked = decltype(masked_tag)::value;
-      const int sb = j % kSBufs, pb = j % kPBufs;
+      const int sb = g % kSBufs, pb = g % kPBufs;
       const uint32_t s_addr = lane_base + 128 * sb;
       const uint32_t sP = smem_u32(smem + L::oP + pb * L::kPBytes) + r * 64;
       const uint32_t sPSF = smem_u32(smem + L::oPSF + pb * L::kPSF) + (r & 31) * 16 + (r >> 5) * 4;
       SAGE3_TRACE_EV(1 + par, j, 0);
-      mbar_wait(&s_full[sb], (uint32_t)(j / kSBufs) & 1u);
+      mbar_wait(&s_full[sb], (uint32_t)(g / kSBufs) & 1u);
       SAGE3_TRACE_EV(1 + par, j, 1);
       tc_fence_after();
       const int kv0 = j * 128;
@@ -557,15 +450,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       float bmax[8];
       auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
+        if constexpr (kSQ) {  // Alg1 L8: S += GEMV(q̄_i, K_j^T), the same 128-vector for every row (broadcast)
+          const uint32_t ds_s = smem_u32(smem + L::oDs + (g % kDsStages) * 512) + c * 128;
+#pragma unroll
+          for (int t = 0; t < 32; t += 4) {
+            float4 g;
+            lds_f4(ds_s + t * 4, g);
+            const f2 lo = fadd2(make_float2(f[t], f[t + 1]), make_float2(g.x, g.y));
+            const f2 hi = fadd2(make_float2(f[t + 2], f[t + 3]), make_float2(g.z, g.w));
+            f[t] = lo.x, f[t + 1] = lo.y, f[t + 2] = hi.x, f[t + 3] = hi.y;
+          }
+        }
         if constexpr (masked) {
 #pragma unroll
           for (int t = 0; t < 32; ++t) f[t] = (32 * c + t > lim) ? -INFINITY : f[t];
         }
-        if constexpr (masked) tmem_st_32x32b_x32(s_addr + 32 * c, v);  // pass 2 reads the final S
+        if constexpr (masked || kSQ) tmem_st_32x32b_x32(s_addr + 32 * c, v);  // pass 2 reads the final S
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
       };
-      {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
+      if constexpr (kSQ) mbar_wait(&ds_full[g % kDsStages], (uint32_t)(g / kDsStages) & 1u);
+      if constexpr (kSQ) {  // two loads in flight (the ds chunk needs registers too)
+        uint32_t va[32], vb[32];
+#pragma unroll
+        for (int c = 0; c < 4; c += 2) {
+          tmem_ld_32x32b_x32(s_addr + 32 * c, va);
+          tmem_ld_32x32b_x32(s_addr + 32 * c + 32, vb);
+          tmem_ld_wait_regs(va);
+          tmem_ld_wait_regs(vb);
+          pass1(c, va);
+          pass1(c + 1, vb);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_empty[g % kDsStages]);  // ds slot read by this warp
+      } else {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
         uint32_t va[32], vb[32], vc[32], vd[32];
         tmem_ld_32x32b_x32(s_addr, va);
         tmem_ld_32x32b_x32(s_addr + 32, vb);
@@ -584,15 +502,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
                                fmaxf(bmax[6], bmax[7]));
       SAGE3_TRACE_EV(par ? 3 : 0, j, 2);
-      const int slot = j % kXSlots;
+      const int slot = g % kXSlots;
       // the exponent reference of this tile's values: tmax_j (two-level: P̃2 = 2688·2^{sl2(S - tmax_j)}) or the
       // running max m_j (direct: P̃ = 2^{sl2(S - m_j)}); the correction warpgroup weights the tile by it
       float eref = tmax;
       if constexpr (kDirect) {
         float mp = -INFINITY;
         if (j > 0) {
-          const int ps = (j - 1) % kXSlots;
-          mbar_wait(&m_full[ps], (uint32_t)((j - 1) / kXSlots) & 1u);
+          const int ps = (g - 1) % kXSlots;
+          mbar_wait(&m_full[ps], (uint32_t)((g - 1) / kXSlots) & 1u);
           mp = lds_f32(xchg_s + ps * 1024);
         }
         eref = fmaxf(mp, tmax);
@@ -600,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&m_full[slot]);  // per thread: orders its own slot write
       }
       const float nb = kDirect ? -eref * sl2 : kLog2_2688 - tmax * sl2;  // P̃2 (P̃) = 2^(S·sl2 + nb)
-      if constexpr (masked) tmem_st_wait();
+      if constexpr (masked || kSQ) tmem_st_wait();
       uint32_t va[32], vb[32];
       tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
       // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
@@ -645,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       SAGE3_TRACE_EV(par ? 3 : 0, j, 4);
       SAGE3_TRACE_EV(1 + par, j, 2);
-      mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
+      mbar_wait(&p_empty[pb], ((uint32_t)(g / kPBufs) & 1u) ^ 1u);
       SAGE3_TRACE_EV(1 + par, j, 3);
       // ---- pass 2: y = P̃2/s, codes E2M1(y), rowsum(P̃2) = Σ_blk s_blk·Σy.  Software-pipelined over the four
       //      32-key chunks: the exp2 of chunk c (MUFU / FMA-pipe polynomial) sits in the same straight-line
@@ -723,28 +641,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (tmax, rowsum) -> correction: every thread releases its own slot writes on x_full, so the hand-off is
       // ordered per thread (compute-sanitizer racecheck clean); P̂2 -> MMA: one arrival per warp after the
       // warp's proxy fences
-#if SAGE3_XFULL_WARP
-      __syncwarp();  // orders the warp's exchange-slot writes before lane 0's release
-      if (lane == 0) {
-        mbar_arrive(&x_full[slot]);
-        mbar_arrive(&p_full[pb]);
-      }
-#else
       mbar_arrive(&x_full[slot]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[pb]);
 #endif
-#endif
       SAGE3_TRACE_WARP(1 + par, j, 4);
     };
-    const int last = nkv - 1;
-    const bool last_masked = last * 128 + 128 > a.N || a.causal;
-    for (int j = par; j < last; j += 2) tile(j, std::false_type{});
-    if ((last & 1) == par) {
-      if (last_masked)
-        tile(last, std::true_type{});
-      else
-        tile(last, std::false_type{});
+    for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
+      q_row = qt * 128 + r;
+      const int last = nkv - 1;
+      const bool last_masked = last * 128 + 128 > a.N || a.causal;
+      for (int j = ((g0 & 1) == par) ? 0 : 1; j < last; j += 2) tile(j, g0 + j, std::false_type{});
+      if (((g0 + last) & 1) == par) {
+        if (last_masked)
+          tile(last, g0 + last, std::true_type{});
+        else
+          tile(last, g0 + last, std::false_type{});
+      }
     }
   } else {
     // -------------------------------------------------------------------- correction + epilogue
@@ -754,20 +667,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     // which is Alg1 L9-L11 up to fp32 rounding: O/l and lse are independent of the reference.
     setmaxnreg_inc<reg_correction<D>()>();
     const int r = threadIdx.x - 128;
-    const int q_row = qt * 128 + r;
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     [[maybe_unused]] const uint32_t xchg_s = smem_u32(smem + L::oXchg) + r * 4;
     const float sl2 = a.scale * kLog2e;
-    float mref = -INFINITY, l = 0.0f;
     f2 o[D / 2];
+    for (int ui = 0, g0 = 0; kPersist ? unit_of(ui) : ui == 0; g0 += nkv, ++ui) {
+    const int q_row = qt * 128 + r;
+    float mref = -INFINITY, l = 0.0f;
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) o[c] = make_float2(0.f, 0.f);
     for (int j = 0; j < nkv; ++j) {
-      const int slot = j % kXSlots, b = j % kSBufs;
+      const int g = g0 + j;
+      const int slot = g % kXSlots, b = g % kSBufs;
       SAGE3_TRACE_EV(4, j, 0);
 #if SAGE3_XCHG_TMEM
       SAGE3_TRACE_EV(4, j, 1);
-      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
+      mbar_wait(&pv_full[b], (uint32_t)(g / kSBufs) & 1u);
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
       uint32_t xv[2];
@@ -777,13 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = __uint_as_float(xv[0]);
       const float rs2 = __uint_as_float(xv[1]);
 #else
-#if SAGE3_CORR_PV_FIRST
-      // PV_j first: its completion implies every softmax thread's x_full arrival (each precedes its warp's p_full
-      // arrival, which precedes the PV MMA), so the x_full wait below never sleeps.  (Waiting on x_full first
-      // sleeps through its 128 per-thread arrivals: ~75 wake-ups per tile per correction warp, ncu r2b.)
-      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
-#endif
-      mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
+      mbar_wait(&x_full[slot], (uint32_t)(g / kXSlots) & 1u);
       SAGE3_TRACE_EV(4, j, 1);
       const float tmax = lds_f32(xchg_s + slot * 1024);
       const float rs2 = lds_f32(xchg_s + slot * 1024 + 512);
@@ -802,9 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!kQSum) l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
 #if !SAGE3_XCHG_TMEM
-#if !SAGE3_CORR_PV_FIRST
-      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
-#endif
+      mbar_wait(&pv_full[b], (uint32_t)(g / kSBufs) & 1u);
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
 #endif
@@ -861,19 +768,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) o[c] = fmul2(o[c], il);
     SAGE3_TRACE_EV(4, 126, 1);
-    // coalesced store: rows -> smem (the K/V rings, idle once the last PV MMA has completed) -> TMA
-    uint8_t* stage = smem + L::oK;
+    // coalesced store: rows -> smem (the K/V rings, idle once the last PV MMA has completed; kPersist: the
+    // dedicated staging buffer, the rings already hold the next unit's tiles) -> TMA
+    uint8_t* stage = smem + (kPersist ? L::oStage : L::oK);
     stage_o_row<D>(stage, r, a.o_dtype, o);
     SAGE3_TRACE_EV(4, 126, 2);
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     SAGE3_TRACE_EV(4, 126, 3);
     if (threadIdx.x == 128) store_o_tile<D>(&tm_o, stage, a.o_dtype, qt * 128, bh % a.H, bh / a.H);
+    if constexpr (kPersist) named_bar_sync(1, 128);  // the store has read the staging buffer (thread 128 waited)
+    }
   }
   SAGE3_TRACE_EV(4, 127, 2);  // correction: epilogue stores issued (thread 128)
   tc_fence_before();
   __syncthreads();
-  if constexpr (kMC) cluster_sync_all();  // the partner's multicasts and commits into this CTA have all landed
   SAGE3_TRACE_EV(0, 127, 3);  // all roles done
   if (warp == 2) {
     tc_fence_after();
@@ -882,15 +791,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------- host
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kPersist>
 cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D, kMX, kQSum, kSQ>;
+  using L = Layout<D, kMX, kQSum, kPersist>;
   static std::atomic<bool> attr_done[64];  // one-time attribute setup per device (racing callers both set it: idempotent)
+  static int n_sm[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum, kPersist>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
     if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
     attr_done[dev] = true;
   }
   const int BH = a.B * a.H;
@@ -902,94 +814,31 @@ cudaError_t launch_dk(const AttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   const int64_t units = a.unit_end - a.unit_begin;
   if (units <= 0) return cudaSuccess;
-  attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum><<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
+  const int64_t sms = dev < 64 && n_sm[dev] > 0 ? n_sm[dev] : 148;
+  const unsigned grid = (unsigned)(kPersist ? (units < sms ? units : sms) : units);
+  attn_fwd_kernel<D, kSQ, kMX, kDirect, kEarly, kQSum, kPersist><<<grid, kThreads, L::kSmemAlloc, stream>>>(
+      tq, tk, tv, to, a);
   return cudaGetLastError();
-}
-
-// K/V tile sharing in 2-CTA clusters (kMC): non-causal north_star path, pairs of adjacent query tiles of one head.
-template <int D>
-cudaError_t launch_mc(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D, false, false, false>;
-  auto kern = attn_fwd_kernel<D, false, false, false, false, false, true>;
-  static std::atomic<bool> attr_done[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
-    if (e != cudaSuccess) return e;
-    attr_done[dev] = true;
-  }
-  const int BH = a.B * a.H;
-  CUtensorMap tq, tk, tv, to;
-  if (!make_map(&tq, a.q_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
-      !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 64) ||  // half K tiles
-      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D / 2) ||  // half Vᵀ tiles
-      !make_map_o(&to, a.o, a.o_dtype, a.B, a.H, a.N, D, a.o_sb, a.o_sh, a.o_sn))
-    return cudaErrorInvalidValue;
-  const int64_t units = a.unit_end - a.unit_begin;
-  if (units <= 0) return cudaSuccess;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)units, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = L::kSmemAlloc;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, a);
-}
-bool kv_multicast_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("SAGE3_KV_MULTICAST");
-    return e != nullptr && e[0] == '1';
-  }();
-  return on;
-}
-
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kQSum = false>
-cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
-  if constexpr (!kSQ && !kMX && !kDirect && !kQSum) {
-    if (kv_multicast_enabled() && !a.causal && (a.Np / 128) % 2 == 0 && a.unit_begin % 2 == 0 &&
-        (a.unit_end - a.unit_begin) % 2 == 0)
-      return launch_mc<D>(a, stream);
-  }
-  if constexpr (!kDirect) {  // the north_star path (and smoothing Q): long sequences take the early-TMA instantiation
-    if (SAGE3_EARLY_TMA && a.N >= kEarlyMinN) return launch_dk<D, kSQ, kMX, kDirect, true, kQSum>(a, stream);
-  }
-  return launch_dk<D, kSQ, kMX, kDirect, false, kQSum>(a, stream);
 }
 
 }  // namespace
 
-template <bool kMX>
-cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
-  if (a.p_direct) {  // ablation: no smoothing-Q instantiation (rejected in abi.cu)
-    return a.d == 128 ? launch_d<128, false, kMX, true>(a, stream) : launch_d<64, false, kMX, true>(a, stream);
-  }
-  if constexpr (!kMX) {  // NEXT #2 row-sum variant (NVFP4 only, no smoothing Q: rejected in abi.cu)
-    if (a.p_qsum)
-      return a.d == 128 ? launch_d<128, false, false, false, true>(a, stream)
-                        : launch_d<64, false, false, false, true>(a, stream);
-  }
-  if (a.ds) return a.d == 128 ? launch_d<128, true, kMX, false>(a, stream) : launch_d<64, true, kMX, false>(a, stream);
-  if (!kMX && attention_persist_enabled(a)) return launch_attention_persist(a, stream);
-  if (!kMX && attention3_enabled(a.d, a.N, a.causal)) return launch_attention3(a, stream);
-  return a.d == 128 ? launch_d<128, false, kMX, false>(a, stream) : launch_d<64, false, kMX, false>(a, stream);
-}
-
-cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream) {
-  return a.mx ? launch_fmt<true>(a, stream) : launch_fmt<false>(a, stream);
-}
-
-#ifdef SAGE3_TRACE
-extern "C" int sage3_debug_trace_copy(void* host, size_t bytes) {
-  if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);
-  return (int)cudaMemcpyFromSymbol(host, g_trace, bytes);
-}
+#ifndef SAGE3_PERSIST_MAX_N
+#define SAGE3_PERSIST_MAX_N 2048  // sequences up to this long run the persistent kernel (0: never)
 #endif
+bool attention_persist_enabled(const AttnArgs& a) {
+  static const bool off = [] {
+    const char* e = std::getenv("SAGE3_PERSIST");
+    return e != nullptr && e[0] == '0';
+  }();
+  // non-causal only: same-box A/B (TOPS, not persistent / persistent) d = 128: 1K 699 / 699, 2K 957 / 987; causal
+  // 1K 373 / 380, 2K 612 / 602; d = 64 causal 2K 332 (attn3.cu) / 299
+  return !off && !a.mx && !a.p_direct && !a.p_qsum && a.ds == nullptr && !a.causal && a.N <= SAGE3_PERSIST_MAX_N;
+}
+
+cudaError_t launch_attention_persist(const AttnArgs& a, cudaStream_t stream) {
+  return a.d == 128 ? launch_dk<128, false, false, false, false, false, true>(a, stream)
+                    : launch_dk<64, false, false, false, false, false, true>(a, stream);
+}
 
 }  // namespace sage3
