@@ -1,6 +1,6 @@
-"""The persistent short-sequence kernel (attn_persist.cu; the default for non-causal N <= 2048) forced for causal
-cases too (SAGE3_PERSIST_MAX_N is compile-time; causal is excluded only by the default selection), and switched off
-(SAGE3_PERSIST=0), each against the oracle through tests/attn_kernel_check.py in its own process."""
+"""The persistent short-sequence kernel (attn_persist.cu; the default for non-causal N <= 2048: the non-causal cases of
+tests/attn_kernel_check.py up to 2100 tokens) and the same cases with it switched off (SAGE3_PERSIST=0), each against
+the oracle in its own process."""
 import os
 import subprocess
 import sys
