@@ -112,9 +112,6 @@ struct AttnArgs {
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream);
 // attn3.cu: the north_star path (NVFP4, two-level P, no smoothing Q) with three softmax warpgroups per CTA.
 bool attention3_enabled(int d, int N, int causal);
-// attn_persist.cu: persistent CTAs for short sequences on the north_star path (SAGE3_PERSIST=0 disables).
-bool attention_persist_enabled(const AttnArgs& a);
-cudaError_t launch_attention_persist(const AttnArgs& a, cudaStream_t stream);
 cudaError_t launch_attention3(const AttnArgs& a, cudaStream_t stream);
 // The NEXT #2 lazy-reference variant (attn_lazy.cu; p_quant = SAGE3_P_TWO_LEVEL_LAZY, no smoothing Q).
 cudaError_t launch_attention_lazy(const AttnArgs& a, cudaStream_t stream);
