@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto issue_s = [&](int j) {  // S_j = FP4MM(Q̂_i, s_Q, K̂_j, s_K) into buffer j%3, once PV_{j-3} has been read
     const int b = j % kBufs, st = j % kKStages;
     A3_EV(threadIdx.x, 5, j, 0);
-    chain_wait(&b_empty[b], ((uint32_t)(j / kBufs) & 1u) ^ 1u);
-    A3_EV(threadIdx.x, 5, j, 1);
+    // s_K first (its columns belong to this buffer, whose previous S MMA has completed), so that only the MMAs
+    // wait for the correction's release of the buffer
     mbar_wait(&k_full[st], (uint32_t)(j / kKStages) & 1u);
     A3_EV(threadIdx.x, 5, j, 2);
     tc_fence_after();
@@ -264,6 +264,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
 #pragma unroll
     for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kSFK + 8 * b + 4 * at, sf_desc(sKSF + 512 * at));
+    chain_wait(&b_empty[b], ((uint32_t)(j / kBufs) & 1u) ^ 1u);
+    A3_EV(threadIdx.x, 5, j, 1);
+    tc_fence_after();
 #pragma unroll
     for (int ks = 0; ks < D / 64; ++ks) {
       const uint64_t ad = make_smem_desc(smem_u32(smem + L::oQ) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
