@@ -60,6 +60,9 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_XCHG_TMEM
 #define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
 #endif
+#ifndef SAGE3_SF_EARLY
+#define SAGE3_SF_EARLY 1  // 1: the S issuer copies s_K before waiting for the buffer (as attn3.cu; +0.7% at N = 32K)
+#endif
 #ifndef SAGE3_XFULL_WARP
 #define SAGE3_XFULL_WARP 0  // 1: one x_full arrival per softmax warp (after __syncwarp) instead of one per thread
 #endif
@@ -438,6 +441,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_s = [&](int j) {
           const int b = j % kSBufs, st = j % kKStages;
           SAGE3_TRACE_EV(5, j, 0);
+#if SAGE3_SF_EARLY
+          // s_K first (tcgen05.cp executes after the previous S MMA, which read the columns): only the MMAs wait
+          // for the correction's release of the buffer
+          mbar_wait(&k_full[st], (uint32_t)(j / kKStages) & 1u);
+          tc_fence_after();
+          const uint8_t* sK = smem + L::oK + st * L::kKSlot;
+          const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
+#pragma unroll
+          for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFK + 4 * at, sf_desc(sKSF + 512 * at));
+          mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
+          tc_fence_after();
+#else
           mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
           SAGE3_TRACE_EV(5, j, 1);
           mbar_wait(&k_full[st], (uint32_t)(j / kKStages) & 1u);
@@ -447,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
 #pragma unroll
           for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFK + 4 * at, sf_desc(sKSF + 512 * at));
+#endif
 #pragma unroll
           for (int ks = 0; ks < D / 64; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sQ) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
