@@ -60,6 +60,12 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_XCHG_TMEM
 #define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
 #endif
+#ifndef SAGE3_PV_SF_EARLY
+#define SAGE3_PV_SF_EARLY 0  // 1: the PV issuer copies s_V before waiting for P̂2
+#endif
+#ifndef SAGE3_EARLY_RELEASE
+#define SAGE3_EARLY_RELEASE 0  // 1: the correction releases the S/PV buffer before the last chunk's FFMA2s
+#endif
 #ifndef SAGE3_SF_EARLY
 #define SAGE3_SF_EARLY 1  // 1: the S issuer copies s_K before waiting for the buffer (as attn3.cu; +0.7% at N = 32K)
 #endif
@@ -488,20 +494,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_pv = [&](int j) {
           const int b = j % kSBufs, pb = j % kPBufs, st = j % kVStages;
           SAGE3_TRACE_EV(6, j, 0);
+          const uint8_t* sP = smem + L::oP + pb * L::kPBytes;
+          const uint8_t* sV = smem + L::oV + st * L::kVBytes;
+          const uint8_t* sPSF = smem + L::oPSF + pb * L::kPSF;
+          const uint8_t* sVSF = smem + L::oVSF + st * L::kVSF;
+#if SAGE3_PV_SF_EARLY
+          // s_V first (ordered after the previous PV MMA, which read the columns): only s_P2 and the MMAs wait for P̂2
+          mbar_wait(&v_full[st], (uint32_t)(j / kVStages) & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int at = 0; at < kPVAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFV + 4 * at, sf_desc(sVSF + 512 * at));
+          mbar_wait(&p_full[pb], (uint32_t)(j / kPBufs) & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int at = 0; at < kPVAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFP + 4 * at, sf_desc(sPSF + 512 * at));
+#else
           mbar_wait(&p_full[pb], (uint32_t)(j / kPBufs) & 1u);
           SAGE3_TRACE_EV(6, j, 1);
           mbar_wait(&v_full[st], (uint32_t)(j / kVStages) & 1u);
           SAGE3_TRACE_EV(6, j, 2);
           tc_fence_after();
-          const uint8_t* sP = smem + L::oP + pb * L::kPBytes;
-          const uint8_t* sV = smem + L::oV + st * L::kVBytes;
-          const uint8_t* sPSF = smem + L::oPSF + pb * L::kPSF;
-          const uint8_t* sVSF = smem + L::oVSF + st * L::kVSF;
 #pragma unroll
           for (int at = 0; at < kPVAtoms; ++at) {
             tmem_cp_32x128b_x4(tbase + kColSFP + 4 * at, sf_desc(sPSF + 512 * at));
             tmem_cp_32x128b_x4(tbase + kColSFV + 4 * at, sf_desc(sVSF + 512 * at));
           }
+#endif
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sP) + 32 * ks, 16, 512, kLayoutSw64);
@@ -860,12 +878,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[kPVC];
         tmem_ld_cols(pv_base + kPVC * c, v);
         tmem_ld_wait_regs(v);
+#if SAGE3_EARLY_RELEASE
+        if (c == D / kPVC - 1) {  // the last chunk is in registers: release the buffer before its FFMA2s
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&b_empty[b]);
+        }
+#endif
         acc(c, v);
       }
 #endif
+#if !SAGE3_EARLY_RELEASE
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&b_empty[b]);
+#endif
       SAGE3_TRACE_EV(4, j, 3);
     }
     const float m = mref;
@@ -992,6 +1019,7 @@ cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
                         : launch_d<64, false, false, false, true>(a, stream);
   }
   if (a.ds) return a.d == 128 ? launch_d<128, true, kMX, false>(a, stream) : launch_d<64, true, kMX, false>(a, stream);
+  if (!kMX && !a.causal && attention5_enabled()) return launch_attention5(a, stream);
   if (!kMX && attention3_enabled(a.d, a.N, a.causal)) return launch_attention3(a, stream);
   return a.d == 128 ? launch_d<128, false, kMX, false>(a, stream) : launch_d<64, false, kMX, false>(a, stream);
 }

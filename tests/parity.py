@@ -74,8 +74,9 @@ def vmax_of(head) -> float:
     return float(np.abs(oracle.dequant_fmt(head.v_codes, head.v_sf, head.fmt)).max())
 
 
-def oracle_attention(heads, *, causal, scale, rows=None, p_mode=None, want_lse=False):
+def oracle_attention(heads, *, causal, scale, rows=None, p_mode=None, want_lse=False, bkv=128):
     """oracle.attn_fwd with the decision-sensitivity output; returns (O, lse, amb, vmax per head)."""
     kw = {} if p_mode is None else {"p_mode": p_mode}
+    kw["bkv"] = bkv
     O, lse, amb = oracle.attn_fwd(heads, causal=causal, scale=scale, rows=rows, amb_delta=AMB_DELTA, **kw)
     return O, lse, amb, [vmax_of(h) for h in heads]
