@@ -1019,7 +1019,6 @@ cudaError_t launch_fmt(const AttnArgs& a, cudaStream_t stream) {
                         : launch_d<64, false, false, false, true>(a, stream);
   }
   if (a.ds) return a.d == 128 ? launch_d<128, true, kMX, false>(a, stream) : launch_d<64, true, kMX, false>(a, stream);
-  if (!kMX && !a.causal && attention5_enabled()) return launch_attention5(a, stream);
   if (!kMX && attention3_enabled(a.d, a.N, a.causal)) return launch_attention3(a, stream);
   return a.d == 128 ? launch_d<128, false, kMX, false>(a, stream) : launch_d<64, false, kMX, false>(a, stream);
 }

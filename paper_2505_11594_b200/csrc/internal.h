@@ -112,9 +112,6 @@ struct AttnArgs {
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t stream);
 // attn3.cu: the north_star path (NVFP4, two-level P, no smoothing Q) with three softmax warpgroups per CTA.
 bool attention3_enabled(int d, int N, int causal);
-// attn5.cu: B_kv = 64, three softmax warpgroups, separate PV slots (experiment: SAGE3_ATTN_KERNEL=5, non-causal).
-bool attention5_enabled();
-cudaError_t launch_attention5(const AttnArgs& a, cudaStream_t stream);
 cudaError_t launch_attention3(const AttnArgs& a, cudaStream_t stream);
 // The NEXT #2 lazy-reference variant (attn_lazy.cu; p_quant = SAGE3_P_TWO_LEVEL_LAZY, no smoothing Q).
 cudaError_t launch_attention_lazy(const AttnArgs& a, cudaStream_t stream);
