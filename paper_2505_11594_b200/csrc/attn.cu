@@ -60,6 +60,9 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_XCHG_TMEM
 #define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
 #endif
+#ifndef SAGE3_CORR_BACKOFF_NS
+#define SAGE3_CORR_BACKOFF_NS 0  // > 0: the correction polls x_full with this nanosleep between probes
+#endif
 #ifndef SAGE3_PV_SF_EARLY
 #define SAGE3_PV_SF_EARLY 0  // 1: the PV issuer copies s_V before waiting for P̂2
 #endif
@@ -817,7 +820,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // sleeps through its 128 per-thread arrivals: ~75 wake-ups per tile per correction warp, ncu r2b.)
       mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
 #endif
+#if SAGE3_CORR_BACKOFF_NS
+      // probe + timed nap instead of the suspend-until-event wait, which wakes on each of the 128 per-thread arrivals
+      while (!mbar_test_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u)) __nanosleep(SAGE3_CORR_BACKOFF_NS);
+#else
       mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
+#endif
       SAGE3_TRACE_EV(4, j, 1);
       const float tmax = lds_f32(xchg_s + slot * 1024);
       const float rs2 = lds_f32(xchg_s + slot * 1024 + 512);
