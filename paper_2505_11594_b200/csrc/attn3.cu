@@ -4,10 +4,9 @@
 //
 // Why: attn.cu's softmax is latency-bound — two softmax warps per SM sub-partition cannot keep MUFU and the
 // issue port busy through the pass-1 / block-scale chains (ncu: issue 63%, MUFU 56%).  The
-// register file decides how many softmax warps fit: attn.cu spends one warpgroup (32 registers) on the TMA and
-// MMA issuers and one (192) on the correction.  Here the issuers live inside the correction warpgroup — each of
-// its four warps owns 32 query rows of O and one issuer role on an elected lane — which frees a warpgroup slot
-// for a third softmax warpgroup (176 + 3 x 112 = 512 registers per lane slot).
+// register file decides how many softmax warps fit: attn.cu spends one warpgroup (32 registers) on single-lane TMA
+// and MMA issuers and one (192) on the correction.  Here the issue roles are folded into warps that would otherwise
+// wait, which frees a warpgroup slot for a third softmax warpgroup (176 + 3 x 112 = 512 registers per lane slot).
 //
 // One CTA = one 128-row query tile Q_i of one (b,h); loop over 128-key tiles j (B_q = B_kv = 128).
 //   WG0 (warps 0-3): correction rows 32w..32w+31 (O in registers, Alg1 L9-L11, L13, the epilogue); thread 0 also
@@ -23,12 +22,11 @@
 //                                         with tile j (shared-memory counter, acq_rel atomics).
 // Per tile j the correction warps do O += w_j PV_j; warps 1 and 2 of the softmax warpgroup refill the K / V ring
 // slots (tiles j + kKStages / j + 2) as soon as S_j is complete — the slot reuse is implied by the S/PV chain, so no
-// ring has an "empty" barrier.  (With the refills on correction warps, the refilling warp fell ~3000 cycles behind
-// the other three and paced the chain: 2250 cycles per tile.)  Measured alternatives: issuing from fixed correction warps (their per-tile loop then
-// serialises PV issue, O update and S issue): 2085 cycles per tile; PV from warp 0 of each softmax warpgroup after
-// waiting for the others (the leader lags its warpgroup): 1680; S by the 4th correction warp done with PV_{j-3} (a
-// tcgen05.ld issued after a tcgen05.mma by the same warp waits for the MMA, so the issuing warp falls a tile behind
-// and stays last): 1880.
+// ring has an "empty" barrier.  Measured alternatives (cycles per tile at N = 16K): refills on
+// correction warps (the refilling warp falls ~3000 cycles behind and paces the chain) 2250; all issue roles on fixed
+// correction warps (their per-tile loop serialises PV issue, O update and S issue) 2085; PV from warp 0 of each
+// softmax warpgroup after waiting for the others (the leader lags its warpgroup) 1680; S by the 4th correction warp
+// done with PV_{j-3} (a tcgen05.ld issued after a tcgen05.mma by the same warp waits for the MMA) 1880.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
