@@ -219,7 +219,7 @@ struct Layout {
 // RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
 // of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
 // warpgroups are no longer independent in this mode.
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kMC = false, bool kSX = false>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kMC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -774,146 +774,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       SAGE3_TRACE_WARP(1 + par, j, 4);
     };
-    // kSX (north_star two-level only): exps relative to each 16-key block's own max in pass A, while the block
-    // maxima are taken — e1 = 2^{sl2 (S − bmax_blk)} (MUFU / polynomial) and Σ e1 per block, written back over S in
-    // TMEM — then, once tmax and the E4M3 block scales are known, pass B forms y = P̃2/s = e1·F_blk with
-    // F_blk = 2^{sl2 (bmax_blk − tmax) + log2 2688 − log2 s_blk} (FMUL2) and the codes; rowsum(P̃2) =
-    // Σ_blk s_blk F_blk Σe1.  The same quantities as tile() up to rounding (one extra product per element); the
-    // MUFU work moves from after the block-scale chain into the pass that takes the maxima.
-    auto tile_sx = [&](const int j, auto masked_tag) {
-      constexpr bool masked = decltype(masked_tag)::value;
-      const int sb = j % kSBufs, pb = j % kPBufs;
-      const uint32_t s_addr = lane_base + 128 * sb;
-      const uint32_t sP = smem_u32(smem + L::oP + pb * L::kPBytes) + r * 64;
-      const uint32_t sPSF = smem_u32(smem + L::oPSF + pb * L::kPSF) + (r & 31) * 16 + (r >> 5) * 4;
-      mbar_wait(&s_full[sb], (uint32_t)(j / kSBufs) & 1u);
-      tc_fence_after();
-      const int kv0 = j * 128;
-      const int lim = a.causal ? min(a.N - 1, q_row) - kv0 : a.N - 1 - kv0;
-      float bmax[8], bsum[8];
-      // ---- pass A per 32-key chunk c (blocks 2c, 2c+1)
-      auto pass_a = [&](int c, uint32_t(&v)[32]) {
-        float* f = reinterpret_cast<float*>(v);
-        if constexpr (masked) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) f[t] = (32 * c + t > lim) ? -INFINITY : f[t];
-        }
-        const float b0 = max16(f), b1 = max16(f + 16);
-        bmax[2 * c] = b0;
-        bmax[2 * c + 1] = b1;
-        // -bmax·sl2 (a fully masked block: -inf max -> a huge finite offset, e1 = 2^-inf = 0)
-        const f2 nab = fmul2(make_float2(fmaxf(b0, -1e30f), fmaxf(b1, -1e30f)), make_float2(-sl2, -sl2));
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {  // e1 in place of S
-          const float nbh = i < 8 ? nab.x : nab.y;
-          const f2 x = ffma2(make_float2(f[2 * i], f[2 * i + 1]), sl2x2, make_float2(nbh, nbh));
-          const f2 e = ((poly_mask<false>() >> i) & 1u) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          f[2 * i] = e.x;
-          f[2 * i + 1] = e.y;
-        }
-#pragma unroll
-        for (int hb = 0; hb < 2; ++hb) {
-          const float* ee = f + 16 * hb;
-          const f2 s01 = fadd2(fadd2(make_float2(ee[0], ee[1]), make_float2(ee[2], ee[3])),
-                               fadd2(make_float2(ee[4], ee[5]), make_float2(ee[6], ee[7])));
-          const f2 s23 = fadd2(fadd2(make_float2(ee[8], ee[9]), make_float2(ee[10], ee[11])),
-                               fadd2(make_float2(ee[12], ee[13]), make_float2(ee[14], ee[15])));
-          const f2 sy = fadd2(s01, s23);
-          bsum[2 * c + hb] = sy.x + sy.y;
-        }
-        tmem_st_32x32b_x32(s_addr + 32 * c, v);
-      };
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {  // the e1 store reads its registers until wait::st
-        uint32_t va[32];
-        tmem_ld_32x32b_x32(s_addr + 32 * c, va);
-        tmem_ld_wait_regs(va);
-        pass_a(c, va);
-        tmem_st_wait();
-      }
-      const float tmax = fmax3(fmax3(bmax[0], bmax[1], bmax[2]), fmax3(bmax[3], bmax[4], bmax[5]),
-                               fmaxf(bmax[6], bmax[7]));
-      const float nb = kLog2_2688 - tmax * sl2;
-      // block scales exactly as tile(): s = E4M3(2^(bmax·sl2 + nb) / 6); F = 2^(bmax·sl2 + nb - log2 s)
-      float fblk[8], sdec[8];
-      uint32_t scw[2];
-      {
-        uint32_t c2[4];
-        float eb[8];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const f2 e2 = ffma2(make_float2(bmax[2 * k], bmax[2 * k + 1]), sl2x2, make_float2(nb, nb));
-          eb[2 * k] = e2.x, eb[2 * k + 1] = e2.y;
-          const f2 q = fmul2(make_float2(ex2(e2.x), ex2(e2.y)), make_float2(kOneSixth, kOneSixth));
-          c2[k] = cvt_e4m3x2(q.x, q.y);
-        }
-        scw[0] = __byte_perm(c2[0], c2[1], 0x5410);
-        scw[1] = __byte_perm(c2[2], c2[3], 0x5410);
-#pragma unroll
-        for (int blk = 0; blk < 8; ++blk) {
-          const float2 t = s_lut[(scw[blk >> 2] >> (8 * (blk & 3))) & 0xFFu];
-          fblk[blk] = ex2(eb[blk] + t.x);
-          sdec[blk] = t.y;
-        }
-      }
-      float rowsum = 0.0f;
-#pragma unroll
-      for (int blk = 0; blk < 8; ++blk) rowsum = fmaf(sdec[blk] * fblk[blk], bsum[blk], rowsum);
-      tmem_st_wait();
-      mbar_wait(&p_empty[pb], ((uint32_t)(j / kPBufs) & 1u) ^ 1u);
-      // ---- pass B: y = e1·F, E2M1 codes, P̂2 -> smem
-      auto pass_b = [&](int c, const uint32_t(&v)[32]) {
-        const f2 fA = make_float2(fblk[2 * c], fblk[2 * c]), fB = make_float2(fblk[2 * c + 1], fblk[2 * c + 1]);
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const f2 fq = q < 2 ? fA : fB;
-          f2 y[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            y[i] = fmul2(make_float2(__uint_as_float(v[8 * q + 2 * i]), __uint_as_float(v[8 * q + 2 * i + 1])), fq);
-          w[q] = cvt_e2m1x8(y[0].x, y[0].y, y[1].x, y[1].y, y[2].x, y[2].y, y[3].x, y[3].y);
-        }
-        sts_v4(sP + ((c ^ ((r >> 1) & 3)) * 16), w[0], w[1], w[2], w[3]);
-      };
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t va[32];
-        tmem_ld_32x32b_x32(s_addr + 32 * c, va);
-        tmem_ld_wait_regs(va);
-        pass_b(c, va);
-      }
-      sts_u32(sPSF, scw[0]);
-      sts_u32(sPSF + 512, scw[1]);
-      const int slot = j % kXSlots;
-      sts_f32(xchg_s + slot * 1024, tmax);
-      sts_f32(xchg_s + slot * 1024 + 512, rowsum);
-      tc_fence_before();
-      fence_proxy_async_smem();
-      mbar_arrive(&x_full[slot]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[pb]);
-    };
-    if constexpr (kSX) {
-      const int last = nkv - 1;
-      const bool last_masked = last * 128 + 128 > a.N || a.causal;
-      for (int j = par; j < last; j += 2) tile_sx(j, std::false_type{});
-      if ((last & 1) == par) {
-        if (last_masked)
-          tile_sx(last, std::true_type{});
-        else
-          tile_sx(last, std::false_type{});
-      }
-    } else {
-      const int last = nkv - 1;
-      const bool last_masked = last * 128 + 128 > a.N || a.causal;
-      for (int j = par; j < last; j += 2) tile(j, std::false_type{});
-      if ((last & 1) == par) {
-        if (last_masked)
-          tile(last, std::true_type{});
-        else
-          tile(last, std::false_type{});
-      }
+    const int last = nkv - 1;
+    const bool last_masked = last * 128 + 128 > a.N || a.causal;
+    for (int j = par; j < last; j += 2) tile(j, std::false_type{});
+    if ((last & 1) == par) {
+      if (last_masked)
+        tile(last, std::true_type{});
+      else
+        tile(last, std::false_type{});
     }
   } else {
     // -------------------------------------------------------------------- correction + epilogue
@@ -1125,38 +993,6 @@ cudaError_t launch_mc(const AttnArgs& a, cudaStream_t stream) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, a);
 }
-// kSX: the split-exp softmax (tile_sx), SAGE3_SPLIT_EXP=1 (north_star two-level path).
-template <int D>
-cudaError_t launch_sx(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D, false, false, false>;
-  auto kern = attn_fwd_kernel<D, false, false, false, true, false, false, true>;
-  static std::atomic<bool> attr_done[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
-    if (e != cudaSuccess) return e;
-    attr_done[dev] = true;
-  }
-  const int BH = a.B * a.H;
-  CUtensorMap tq, tk, tv, to;
-  if (!make_map(&tq, a.q_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
-      !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
-      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D) ||
-      !make_map_o(&to, a.o, a.o_dtype, a.B, a.H, a.N, D, a.o_sb, a.o_sh, a.o_sn))
-    return cudaErrorInvalidValue;
-  const int64_t units = a.unit_end - a.unit_begin;
-  if (units <= 0) return cudaSuccess;
-  kern<<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
-  return cudaGetLastError();
-}
-bool split_exp_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("SAGE3_SPLIT_EXP");
-    return e != nullptr && e[0] == '1';
-  }();
-  return on;
-}
 bool kv_multicast_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("SAGE3_KV_MULTICAST");
@@ -1168,9 +1004,6 @@ bool kv_multicast_enabled() {
 template <int D, bool kSQ, bool kMX, bool kDirect, bool kQSum = false>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
   if constexpr (!kSQ && !kMX && !kDirect && !kQSum) {
-    if constexpr (D == 128) {
-      if (split_exp_enabled()) return launch_sx<D>(a, stream);
-    }
     if (kv_multicast_enabled() && !a.causal && (a.Np / 128) % 2 == 0 && a.unit_begin % 2 == 0 &&
         (a.unit_end - a.unit_begin) % 2 == 0)
       return launch_mc<D>(a, stream);
