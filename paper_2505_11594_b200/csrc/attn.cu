@@ -60,24 +60,6 @@ constexpr int kEarlyMinN = 4096;  // sequences at least this long use the kEarly
 #ifndef SAGE3_XCHG_TMEM
 #define SAGE3_XCHG_TMEM 0  // 1: (eref, rowsum) softmax -> correction through TMEM columns instead of smem + x_full
 #endif
-#ifndef SAGE3_CORR_BACKOFF_NS
-#define SAGE3_CORR_BACKOFF_NS 0  // > 0: the correction polls x_full with this nanosleep between probes
-#endif
-#ifndef SAGE3_PV_SF_EARLY
-#define SAGE3_PV_SF_EARLY 0  // 1: the PV issuer copies s_V before waiting for P̂2
-#endif
-#ifndef SAGE3_EARLY_RELEASE
-#define SAGE3_EARLY_RELEASE 0  // 1: the correction releases the S/PV buffer before the last chunk's FFMA2s
-#endif
-#ifndef SAGE3_SF_EARLY
-#define SAGE3_SF_EARLY 1  // 1: the S issuer copies s_K before waiting for the buffer (as attn3.cu; +0.7% at N = 32K)
-#endif
-#ifndef SAGE3_XFULL_WARP
-#define SAGE3_XFULL_WARP 0  // 1: one x_full arrival per softmax warp (after __syncwarp) instead of one per thread
-#endif
-#ifndef SAGE3_CORR_PV_FIRST
-#define SAGE3_CORR_PV_FIRST 0  // 1: the correction waits for PV_j before the (tmax, rowsum) exchange of tile j
-#endif
 #ifndef SAGE3_PROD_BACKOFF
 #define SAGE3_PROD_BACKOFF 0  // 1: TMA producers poll their empty barriers with test_wait + timed sleep
 #endif
@@ -281,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[b], 4);  // one arrival per softmax warp
       mbar_init(&p_empty[b], 1);
     }
-    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], SAGE3_XFULL_WARP ? 4 : 128);
+    for (int s = 0; s < kXSlots; ++s) mbar_init(&x_full[s], 128);
     for (int s = 0; s < kXSlots; ++s) mbar_init(&m_full[s], 128);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
@@ -450,7 +432,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_s = [&](int j) {
           const int b = j % kSBufs, st = j % kKStages;
           SAGE3_TRACE_EV(5, j, 0);
-#if SAGE3_SF_EARLY
           // s_K first (tcgen05.cp executes after the previous S MMA, which read the columns): only the MMAs wait
           // for the correction's release of the buffer
           mbar_wait(&k_full[st], (uint32_t)(j / kKStages) & 1u);
@@ -461,17 +442,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFK + 4 * at, sf_desc(sKSF + 512 * at));
           mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
           tc_fence_after();
-#else
-          mbar_wait(&b_empty[b], ((uint32_t)(j / kSBufs) & 1u) ^ 1u);
-          SAGE3_TRACE_EV(5, j, 1);
-          mbar_wait(&k_full[st], (uint32_t)(j / kKStages) & 1u);
-          SAGE3_TRACE_EV(5, j, 2);
-          tc_fence_after();
-          const uint8_t* sK = smem + L::oK + st * L::kKSlot;
-          const uint8_t* sKSF = smem + L::oKSF + st * L::kQKSF;
-#pragma unroll
-          for (int at = 0; at < kQKAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFK + 4 * at, sf_desc(sKSF + 512 * at));
-#endif
 #pragma unroll
           for (int ks = 0; ks < D / 64; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sQ) + 32 * ks, 16, 8 * L::kQKRow, kQKLayout);
@@ -501,17 +471,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint8_t* sV = smem + L::oV + st * L::kVBytes;
           const uint8_t* sPSF = smem + L::oPSF + pb * L::kPSF;
           const uint8_t* sVSF = smem + L::oVSF + st * L::kVSF;
-#if SAGE3_PV_SF_EARLY
-          // s_V first (ordered after the previous PV MMA, which read the columns): only s_P2 and the MMAs wait for P̂2
-          mbar_wait(&v_full[st], (uint32_t)(j / kVStages) & 1u);
-          tc_fence_after();
-#pragma unroll
-          for (int at = 0; at < kPVAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFV + 4 * at, sf_desc(sVSF + 512 * at));
-          mbar_wait(&p_full[pb], (uint32_t)(j / kPBufs) & 1u);
-          tc_fence_after();
-#pragma unroll
-          for (int at = 0; at < kPVAtoms; ++at) tmem_cp_32x128b_x4(tbase + kColSFP + 4 * at, sf_desc(sPSF + 512 * at));
-#else
           mbar_wait(&p_full[pb], (uint32_t)(j / kPBufs) & 1u);
           SAGE3_TRACE_EV(6, j, 1);
           mbar_wait(&v_full[st], (uint32_t)(j / kVStages) & 1u);
@@ -522,7 +481,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_cp_32x128b_x4(tbase + kColSFP + 4 * at, sf_desc(sPSF + 512 * at));
             tmem_cp_32x128b_x4(tbase + kColSFV + 4 * at, sf_desc(sVSF + 512 * at));
           }
-#endif
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             const uint64_t ad = make_smem_desc(smem_u32(sP) + 32 * ks, 16, 512, kLayoutSw64);
@@ -760,17 +718,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (tmax, rowsum) -> correction: every thread releases its own slot writes on x_full, so the hand-off is
       // ordered per thread (compute-sanitizer racecheck clean); P̂2 -> MMA: one arrival per warp after the
       // warp's proxy fences
-#if SAGE3_XFULL_WARP
-      __syncwarp();  // orders the warp's exchange-slot writes before lane 0's release
-      if (lane == 0) {
-        mbar_arrive(&x_full[slot]);
-        mbar_arrive(&p_full[pb]);
-      }
-#else
       mbar_arrive(&x_full[slot]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[pb]);
-#endif
 #endif
       SAGE3_TRACE_WARP(1 + par, j, 4);
     };
@@ -814,18 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float tmax = __uint_as_float(xv[0]);
       const float rs2 = __uint_as_float(xv[1]);
 #else
-#if SAGE3_CORR_PV_FIRST
-      // PV_j first: its completion implies every softmax thread's x_full arrival (each precedes its warp's p_full
-      // arrival, which precedes the PV MMA), so the x_full wait below never sleeps.  (Waiting on x_full first
-      // sleeps through its 128 per-thread arrivals: ~75 wake-ups per tile per correction warp, ncu r2b.)
-      mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
-#endif
-#if SAGE3_CORR_BACKOFF_NS
-      // probe + timed nap instead of the suspend-until-event wait, which wakes on each of the 128 per-thread arrivals
-      while (!mbar_test_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u)) __nanosleep(SAGE3_CORR_BACKOFF_NS);
-#else
       mbar_wait(&x_full[slot], (uint32_t)(j / kXSlots) & 1u);
-#endif
       SAGE3_TRACE_EV(4, j, 1);
       const float tmax = lds_f32(xchg_s + slot * 1024);
       const float rs2 = lds_f32(xchg_s + slot * 1024 + 512);
@@ -844,9 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!kQSum) l = fmaf(w, rs2, l);
       const f2 ww = make_float2(w, w);
 #if !SAGE3_XCHG_TMEM
-#if !SAGE3_CORR_PV_FIRST
       mbar_wait(&pv_full[b], (uint32_t)(j / kSBufs) & 1u);
-#endif
       SAGE3_TRACE_EV(4, j, 2);
       tc_fence_after();
 #endif
@@ -886,21 +823,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[kPVC];
         tmem_ld_cols(pv_base + kPVC * c, v);
         tmem_ld_wait_regs(v);
-#if SAGE3_EARLY_RELEASE
-        if (c == D / kPVC - 1) {  // the last chunk is in registers: release the buffer before its FFMA2s
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&b_empty[b]);
-        }
-#endif
         acc(c, v);
       }
 #endif
-#if !SAGE3_EARLY_RELEASE
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&b_empty[b]);
-#endif
       SAGE3_TRACE_EV(4, j, 3);
     }
     const float m = mref;
