@@ -118,8 +118,14 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
 template <bool kQSum>
 constexpr uint32_t poly_mask() { return kQSum ? SAGE3_POLY_MASK_QS : SAGE3_POLY_MASK_TL; }
 constexpr int kKStages = 4, kVStages = 4;  // (same-box A/B: 4/4 vs 5/4 +0.3% at N = 32K, causal +0.9%; 6/5, 8/6, 4/3, 3/3 slower)
-constexpr int kPBufs = 4;   // P̂2 tiles in smem (tile j -> j % 4)
-constexpr int kXSlots = 8;  // softmax -> correction exchange slots (tile j -> j % 8)
+#ifndef SAGE3_PBUFS
+#define SAGE3_PBUFS 4
+#endif
+constexpr int kPBufs = SAGE3_PBUFS;  // P̂2 tiles in smem (tile j -> j % kPBufs)
+#ifndef SAGE3_XSLOTS
+#define SAGE3_XSLOTS 8
+#endif
+constexpr int kXSlots = SAGE3_XSLOTS;  // softmax -> correction exchange slots (tile j -> j % kXSlots)
 constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
 constexpr int kDsOps = 3;     // smoothing Q: tf32 B operands of the ds MMA (tile j -> j % 3)
 constexpr int kThreads = 512;
