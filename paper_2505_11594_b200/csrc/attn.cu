@@ -123,7 +123,7 @@ constexpr int kKStages = 4, kVStages = 4;  // (same-box A/B: 4/4 vs 5/4 +0.3% at
 #endif
 constexpr int kPBufs = SAGE3_PBUFS;  // P̂2 tiles in smem (tile j -> j % kPBufs)
 #ifndef SAGE3_XSLOTS
-#define SAGE3_XSLOTS 8
+#define SAGE3_XSLOTS 4  // (same-box A/B: 4 vs 8 +0.4% at N = 32K; 3, 6 slower)
 #endif
 constexpr int kXSlots = SAGE3_XSLOTS;  // softmax -> correction exchange slots (tile j -> j % kXSlots)
 constexpr int kDsStages = 4;  // smoothing Q: ds (GEMV term) rows in smem (tile j -> j % 4)
