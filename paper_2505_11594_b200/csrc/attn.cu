@@ -162,7 +162,7 @@ constexpr int kSBufs = 3;
 // TMEM columns per S/PV buffer (tile j -> kColRS + 16 (j % 3)); the ones operand's scale factors sit at kColSF1.
 constexpr uint32_t kColSF1 = 432, kColRS = 448;
 
-template <int D, bool kMX, bool kQSum = false, bool kSQ = false, bool kCP = false>
+template <int D, bool kMX, bool kQSum = false, bool kSQ = false>
 struct Layout {
   static constexpr int kQKRow = D / 2;          // bytes per Q/K row (64 or 32)
   static constexpr int kQBytes = 128 * kQKRow;   // Q tile codes
@@ -192,10 +192,7 @@ struct Layout {
   // kDsOps B slots of 128 keys x 8 tf32 (32 B per key: [hi, mid, lo, 0] of ds in one 16-byte half, zeros in the other)
   static constexpr int oDsOne = oOnes;
   static constexpr int oDsOp = oDsOne + 4096;
-  // kCP: the block maxima exchange (correction -> softmax): [4 slots][128 rows][8 floats]
-  static constexpr int oBm = ((oDs + kDsStages * 512 + 1023) / 1024) * 1024;
-  static constexpr int oBar =
-      kCP ? oBm + 4 * 4096 : kQSum ? oOnesSF + 1024 : kSQ ? oDsOp + kDsOps * 4096 : oDs + kDsStages * 512;
+  static constexpr int oBar = kQSum ? oOnesSF + 1024 : kSQ ? oDsOp + kDsOps * 4096 : oDs + kDsStages * 512;
   static constexpr int kNumBars =
       1 + 2 * kKStages + 2 * kVStages + 3 * kSBufs + 2 * kPBufs + 2 * kXSlots + 2 * kDsStages + 2 * kDsOps;
   static constexpr int oTmem = oBar + kNumBars * 8;
@@ -212,12 +209,12 @@ struct Layout {
 // RUNNING max m_j and s_P1 = 1, instead of the two-level form.  m_j is a chain through the tiles: the warpgroup
 // of tile j waits for m_{j-1} from the other one (published right after its pass 1), so the two softmax
 // warpgroups are no longer independent in this mode.
-template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kMC = false, bool kCP = false>
+template <int D, bool kSQ, bool kMX, bool kDirect, bool kEarly, bool kQSum, bool kMC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                     const AttnArgs a) {
-  using L = Layout<D, kMX, kQSum, kSQ, kCP>;
+  using L = Layout<D, kMX, kQSum, kSQ>;
   extern __shared__ uint8_t smem_raw[];
   // (-log2 s, s) per E4M3 scale code (static shared memory: LDS.64 with an immediate address)
   __shared__ __align__(1024) float2 s_lut[128];
@@ -238,8 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_empty = p_full + kPBufs;    // MMA -> softmax: PV_j done with smem buffer j%4
   uint64_t* x_full = p_empty + kPBufs;    // softmax -> correction: (tmax_j, rowsum P̃2_j) in slot j%8 (smem mode)
   uint64_t* ds_full = x_full + kXSlots;   // smoothing Q: ds row of tile j in slot j%4 (bulk copy)
-  uint64_t* ds_empty = ds_full + kDsStages;  // (unused; kCP: the block-maxima exchange, slot t%4, 128 arrivals)
-  [[maybe_unused]] uint64_t* bm_full = ds_empty;
+  uint64_t* ds_empty = ds_full + kDsStages;  // (unused)
   uint64_t* m_full = ds_empty + kDsStages;    // direct P: m_j of tile j in xchg slot j%8 (softmax -> softmax)
   uint64_t* dsop_full = m_full + kXSlots;     // smoothing Q: V-producer warp -> MMA: tf32 ds operand of tile j in slot j%3
   uint64_t* dsop_empty = dsop_full + kDsOps;  // MMA -> V-producer warp: the ds MMA of tile j read slot j%3
@@ -279,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kXSlots; ++s) mbar_init(&m_full[s], 128);
     for (int s = 0; s < kDsStages; ++s) {
       mbar_init(&ds_full[s], 1);
-      mbar_init(&ds_empty[s], kCP ? 128 : 1);
+      mbar_init(&ds_empty[s], 1);
     }
     for (int s = 0; s < kDsOps; ++s) {
       mbar_init(&dsop_full[s], 1);
@@ -553,25 +549,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t sP = smem_u32(smem + L::oP + pb * L::kPBytes) + r * 64;
       const uint32_t sPSF = smem_u32(smem + L::oPSF + pb * L::kPSF) + (r & 31) * 16 + (r >> 5) * 4;
       SAGE3_TRACE_EV(1 + par, j, 0);
-      float bmax[8];
-      if constexpr (kCP) {  // block maxima (and the masked write-back) from the correction warpgroup
-        mbar_wait(&bm_full[j & 3], (uint32_t)(j >> 2) & 1u);
-        tc_fence_after();
-        float4 b0, b1;
-        lds_f4(smem_u32(smem + L::oBm + (j & 3) * 4096) + r * 32, b0);
-        lds_f4(smem_u32(smem + L::oBm + (j & 3) * 4096) + r * 32 + 16, b1);
-        bmax[0] = b0.x, bmax[1] = b0.y, bmax[2] = b0.z, bmax[3] = b0.w;
-        bmax[4] = b1.x, bmax[5] = b1.y, bmax[6] = b1.z, bmax[7] = b1.w;
-      } else {
       mbar_wait(&s_full[sb], (uint32_t)(j / kSBufs) & 1u);
       SAGE3_TRACE_EV(1 + par, j, 1);
       tc_fence_after();
-      }
       const int kv0 = j * 128;
       const int lim = a.causal ? min(a.N - 1, q_row) - kv0 : a.N - 1 - kv0;  // last visible key in tile
       // ---- pass 1: 16-key block maxima of S (reused for the row max and for s_P2).  Masked keys are set
       //      to -inf and written back to TMEM so pass 2 needs no masking code.  All four 32-column TMEM
       //      loads are in flight together (one round trip; the pass-2 buffers are not live yet).
+      float bmax[8];
       auto pass1 = [&](int c, uint32_t(&v)[32]) {
         float* f = reinterpret_cast<float*>(v);
         if constexpr (masked) {
@@ -582,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         bmax[2 * c] = max16(f);
         bmax[2 * c + 1] = max16(f + 16);
       };
-      if constexpr (!kCP) {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
+      {  // all four 32-column loads in flight (the pass-2 buffers are not live yet)
         uint32_t va[32], vb[32], vc[32], vd[32];
         tmem_ld_32x32b_x32(s_addr, va);
         tmem_ld_32x32b_x32(s_addr + 32, vb);
@@ -617,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&m_full[slot]);  // per thread: orders its own slot write
       }
       const float nb = kDirect ? -eref * sl2 : kLog2_2688 - tmax * sl2;  // P̃2 (P̃) = 2^(S·sl2 + nb)
-      if constexpr (masked && !kCP) tmem_st_wait();
+      if constexpr (masked) tmem_st_wait();
       uint32_t va[32], vb[32];
       tmem_ld_32x32b_x32(s_addr, va);  // pass-2 chunk 0, overlapped with the block-scale math below
       // ---- block scales of φ(P̃2): amax_blk = 2^(bmax·sl2 + nb) (the argmax element's own value),
@@ -771,57 +757,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     f2 o[D / 2];
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) o[c] = make_float2(0.f, 0.f);
-    // kCP: this warpgroup takes the softmax's pass 1 two tiles ahead — the 16-key block maxima of S_t (masked keys
-    // set to -inf and written back for the masked last tile), published to the softmax through smem slot t%4
-    [[maybe_unused]] auto cpass1 = [&](int t) {
-      const int sbt = t % kSBufs;
-      mbar_wait(&s_full[sbt], (uint32_t)(t / kSBufs) & 1u);
-      tc_fence_after();
-      const uint32_t s_addr = lane_base + 128 * sbt;
-      const int lim = a.causal ? min(a.N - 1, q_row) - t * 128 : a.N - 1 - t * 128;
-      // warp-uniform (tcgen05.st is warp-collective): only the last tile can need masking
-      const bool masked = t == nkv - 1 && (nkv * 128 > a.N || a.causal);
-      float bm[8];
-      uint32_t va[16], vb[16];
-      tmem_ld_32x32b_x16(s_addr, va);
-#pragma unroll
-      for (int c = 0; c < 8; c += 2) {
-        tmem_ld_wait_regs(va);
-        tmem_ld_32x32b_x16(s_addr + 16 * (c + 1), vb);
-        float* fa = reinterpret_cast<float*>(va);
-        if (masked) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) fa[k] = (16 * c + k > lim) ? -INFINITY : fa[k];
-          tmem_st_32x32b_x16(s_addr + 16 * c, va);
-        }
-        bm[c] = max16(fa);
-        tmem_ld_wait_regs(vb);
-        if (masked) tmem_st_wait();  // (va is reloaded next)
-        if (c + 2 < 8) tmem_ld_32x32b_x16(s_addr + 16 * (c + 2), va);
-        float* fb = reinterpret_cast<float*>(vb);
-        if (masked) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) fb[k] = (16 * (c + 1) + k > lim) ? -INFINITY : fb[k];
-          tmem_st_32x32b_x16(s_addr + 16 * (c + 1), vb);
-          tmem_st_wait();
-        }
-        bm[c + 1] = max16(fb);
-      }
-      const uint32_t dst = smem_u32(smem + L::oBm + (t & 3) * 4096) + r * 32;
-      sts_v4(dst, __float_as_uint(bm[0]), __float_as_uint(bm[1]), __float_as_uint(bm[2]), __float_as_uint(bm[3]));
-      sts_v4(dst + 16, __float_as_uint(bm[4]), __float_as_uint(bm[5]), __float_as_uint(bm[6]), __float_as_uint(bm[7]));
-      tc_fence_before();
-      mbar_arrive(&bm_full[t & 3]);  // per thread: releases its own slot writes and TMEM stores
-    };
-    if constexpr (kCP) {
-      cpass1(0);
-      if (nkv > 1) cpass1(1);
-    }
     for (int j = 0; j < nkv; ++j) {
       const int slot = j % kXSlots, b = j % kSBufs;
-      if constexpr (kCP) {
-        if (j + 2 < nkv) cpass1(j + 2);
-      }
       SAGE3_TRACE_EV(4, j, 0);
 #if SAGE3_XCHG_TMEM
       SAGE3_TRACE_EV(4, j, 1);
@@ -992,38 +929,6 @@ cudaError_t launch_mc(const AttnArgs& a, cudaStream_t stream) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, a);
 }
-// kCP: the correction warpgroup takes pass 1 (SAGE3_CORR_PASS1=1; north_star two-level path).
-template <int D>
-cudaError_t launch_cp(const AttnArgs& a, cudaStream_t stream) {
-  using L = Layout<D, false, false, false, true>;
-  auto kern = attn_fwd_kernel<D, false, false, false, true, false, false, true>;
-  static std::atomic<bool> attr_done[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
-    if (e != cudaSuccess) return e;
-    attr_done[dev] = true;
-  }
-  const int BH = a.B * a.H;
-  CUtensorMap tq, tk, tv, to;
-  if (!make_map(&tq, a.q_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
-      !make_map(&tk, a.k_data, D / 2, (uint64_t)BH * a.Np, D / 2, 128) ||
-      !make_map(&tv, a.v_data, (uint64_t)a.Np / 2, (uint64_t)BH * D, 64, D) ||
-      !make_map_o(&to, a.o, a.o_dtype, a.B, a.H, a.N, D, a.o_sb, a.o_sh, a.o_sn))
-    return cudaErrorInvalidValue;
-  const int64_t units = a.unit_end - a.unit_begin;
-  if (units <= 0) return cudaSuccess;
-  kern<<<(unsigned)units, kThreads, L::kSmemAlloc, stream>>>(tq, tk, tv, to, a);
-  return cudaGetLastError();
-}
-bool corr_pass1_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("SAGE3_CORR_PASS1");
-    return e != nullptr && e[0] == '1';
-  }();
-  return on;
-}
 bool kv_multicast_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("SAGE3_KV_MULTICAST");
@@ -1035,7 +940,6 @@ bool kv_multicast_enabled() {
 template <int D, bool kSQ, bool kMX, bool kDirect, bool kQSum = false>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
   if constexpr (!kSQ && !kMX && !kDirect && !kQSum) {
-    if (corr_pass1_enabled()) return launch_cp<D>(a, stream);
     if (kv_multicast_enabled() && !a.causal && (a.Np / 128) % 2 == 0 && a.unit_begin % 2 == 0 &&
         (a.unit_end - a.unit_begin) % 2 == 0)
       return launch_mc<D>(a, stream);
