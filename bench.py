@@ -450,7 +450,19 @@ def main():
     traffic, traffic_src = (None, "skipped (--no-traffic)")
     if rank == 0 and world == 1 and not args.no_traffic:
         traffic, traffic_src = measure_traffic(args)
-    roofline = {"bound": "tensor", "kernel": "attn_fwd_kernel<128, 0, 0, 0, 1, %d>" % int(args.p_quant == "qsum"),
+    # the timed instantiation (csrc/attn.cu: D, kSQ, kMX, kDirect, kEarly (N >= 4K), kQSum, kMC; d = 64 with causal masking
+    # or N >= 8K runs attn3.cu's attn3_fwd_kernel<64>)
+    if args.p_quant == "lazy":
+        kname = "attn_lazy_kernel (csrc/attn_lazy.cu)"
+    elif d == 64 and (args.causal or N >= 8192) and args.p_quant in ("two_level",) and not args.smooth_q \
+            and args.fmt == "nvfp4":
+        kname = "attn3_fwd_kernel<64>"
+    else:
+        kname = "attn_fwd_kernel<%d, %d, %d, %d, %d, %d, 0>" % (d, int(args.smooth_q), int(args.fmt == "mxfp4"),
+                                                                 int(args.p_quant == "direct"),
+                                                                 int(N >= 4096 and args.p_quant != "direct"),
+                                                                 int(args.p_quant == "qsum"))
+    roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": attn_tflops, "peak": fp4_peak,
                 "unit": "TFLOP/s", "frac": attn_tflops / fp4_peak, "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_bytes": B * H * N * d * (3 * 0.5 + 3 / 16 + 2),
